@@ -1,0 +1,189 @@
+/* pgg.h — C ABI of the B200 screen-space path-guiding pass (libpgg.so).
+ *
+ * Drop-in boundary for the reference package `pgtrace` (arXiv 2112.09728
+ * desk-scale implementation; paths relative to /root/reference/pkg/src/pgtrace).
+ * The reference exposes Python functions on NumPy arrays and has no FFI of
+ * its own; each entry point below replaces one of them (see INTEGRATION.md
+ * for the ctypes binding that the Python shim uses):
+ *
+ *   pgg_guiding_pass ..... guide_buffers.reproject      guide_buffers.py:78-137
+ *                          guide_buffers.training_pass  guide_buffers.py:262-283
+ *                          ptrace._sample_first_bounce  ptrace.py:161-220 (+ the
+ *                          per-pixel lane setup of ptrace.py:449-475)
+ *                          any subset of the three, fused into one kernel
+ *   pgg_sample_lanes ..... ptrace._sample_first_bounce  ptrace.py:161-220 and
+ *                          mixture.sample_mixture       mixture.py:193-259 on
+ *                          caller-owned PCG32 states (in/out)
+ *   pgg_lobe ............. mixture.lobe_from_stats      mixture.py:129-155
+ *   pgg_trunc_mass ....... mixture.truncation_mass      mixture.py:84-126
+ *   pgg_m_step ........... mixture.m_step_update        mixture.py:276-321
+ *   pgg_make_streams ..... rng.make_streams             rng.py:25-39
+ *   pgg_next_u32 ......... rng.next_u32                 rng.py:42-50
+ *   pgg_frame_key ........ the lane-independent prefix of rng.make_streams
+ *   pgg_pack_* / pgg_gamma_* layout conversion at the API edge
+ *
+ * Conventions: every pointer is a DEVICE pointer owned by the caller unless
+ * stated otherwise; calls are asynchronous on `stream` (a cudaStream_t, NULL =
+ * legacy default stream), keep no global mutable state, never throw, and
+ * return 0 or a pgg_status code.  Safe to call concurrently from several host
+ * threads on different streams.
+ *
+ * Device layouts (P = pixels of a row band, row-major, width = frame width):
+ *   Gamma      two float4 planes  g0 = (mu_x, mu_y, m2_xx, m2_yy)
+ *                                 g1 = (m2_xy, w_sum, pi, k)
+ *   G-buffer   flags u8 (bit0 valid, bit1 has_history, bit2 glossy)
+ *              nd float4 (normal.xyz, depth)      pr float4 (pos.xyz, roughness)
+ *              va float4 (view.xyz, albedo.r)     am float4 (albedo.g, albedo.b, motion.xy)
+ *   VPLs (Pi)  y float4 (pos.xyz, usable = valid && strategy==BRDF ? 1 : 0)
+ *              L float4 (radiance.rgb, 0)
+ *   samples    per lane (pixel*spp + s): dir float4 (wi.xyz world, pdf),
+ *              tag u8 (bit0 strategy GAUSSIAN, bit1 valid)
+ */
+#ifndef PGG_H_
+#define PGG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PGG_ABI_VERSION 1
+
+enum pgg_status {
+  PGG_OK = 0,
+  PGG_ERR_ARGUMENT = 1,    /* bad dimensions / null pointer where required */
+  PGG_ERR_CUDA = 2,        /* kernel launch failed (see pgg_last_cuda_error) */
+  PGG_ERR_UNSUPPORTED = 3  /* device is not sm_100 */
+};
+
+/* A row band [row0, row0 + rows) of a G-buffer in the packed layout. */
+typedef struct pgg_gbuffer {
+  const uint8_t* flags;
+  const float* nd;
+  const float* pr;
+  const float* va;
+  const float* am;
+  int32_t row0;
+  int32_t rows;
+} pgg_gbuffer;
+
+/* Read-only Gamma planes holding rows [row0, row0 + rows). */
+typedef struct pgg_gamma_in {
+  const float* g0;
+  const float* g1;
+  int32_t row0;
+  int32_t rows;
+} pgg_gamma_in;
+
+/* Gamma planes written for the call's own band (cfg.row0, cfg.rows). */
+typedef struct pgg_gamma_out {
+  float* g0;
+  float* g1;
+} pgg_gamma_out;
+
+/* VPL planes holding rows [row0, row0 + rows) (own band + EM halo). */
+typedef struct pgg_vpl {
+  const float* y;
+  const float* L;
+  int32_t row0;
+  int32_t rows;
+} pgg_vpl;
+
+/* Depth-0 samples of the call's own band, lane = pixel * spp + s. */
+typedef struct pgg_samples {
+  float* dir;  /* float4 per lane */
+  uint8_t* tag;
+} pgg_samples;
+
+typedef struct pgg_config {
+  int32_t width, height;       /* full frame */
+  int32_t row0, rows;          /* band produced by this call */
+  int32_t spp;                 /* lanes per pixel (ptrace.py:460-475) */
+  int32_t nee_draws;           /* draws consumed before the depth-0 scatter (3 with NEE + emitters) */
+  int32_t k_max;               /* mixture.KMAX_DEFAULT = 64 */
+  int32_t rotate_mean;         /* ReprojectionPolicy.rotate_mean */
+  double radius;               /* training neighbour radius (guide_buffers.py:19) */
+  double depth_rel_tol;        /* ReprojectionPolicy.depth_rel_tol */
+  double normal_dot_min;       /* ReprojectionPolicy.normal_dot_min */
+  double rough_min_guide;      /* PathConfig.roughness_min_guide */
+  double prev_cam[3];          /* previous frame camera origin (GBuffer.cam_origin) */
+  uint64_t key_sample;         /* pgg_frame_key(seed, frame, 0) */
+  uint64_t key_train;          /* pgg_frame_key(seed, frame, 1) */
+} pgg_config;
+
+/* Fused guiding pass over the band cfg.row0..: for every pixel
+ *   Gamma  = prev ? reproject(gamma_prev, prev, cur) : gamma_prev
+ *   (gamma_reproj) <- Gamma                       if gamma_reproj != NULL
+ *   samples <- depth-0 guided/BRDF sampling       if samples != NULL
+ *   gamma_out <- one EM epoch over the VPL disk   if vpl != NULL (gamma_out required)
+ * gamma_prev / prev must hold every row a motion vector of the band reaches
+ * (reprojection halo); vpl must hold the band +- rint(radius) rows clipped to
+ * the frame (EM halo).  References outside the supplied rows are counted in
+ * *halo_misses (device int32, may be NULL) and treated as out of frame. */
+int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                     const pgg_gamma_in* gamma_prev, const pgg_vpl* vpl, const pgg_gamma_out* gamma_reproj,
+                     const pgg_gamma_out* gamma_out, const pgg_samples* samples, int32_t* halo_misses,
+                     void* stream);
+
+/* Per-lane depth-0 sampling on caller-owned PCG32 states (in/out).
+ * Inputs per lane: normal/view float4 (w unused), roughness, glossy (u8),
+ * guided (u8), pi, lobe float x6 (mu_x, mu_y, l11, l21, l22, trunc_z).
+ * world != 0: lanes are world-space (ptrace._sample_first_bounce: plain lanes
+ * sample the BRDF about `normal`, guided lanes the mixture in its tangent
+ * frame); world == 0: mixture.sample_mixture in the local frame (normal
+ * ignored, `view` holds wo in local coordinates, every lane guided).
+ * Outputs: dir float4 (direction, pdf), tag u8 (bit0 GAUSSIAN, bit1 valid). */
+int pgg_sample_lanes(int64_t n, int32_t world, const float* normal, const float* view, const float* rough,
+                     const uint8_t* glossy, const uint8_t* guided, const float* pi, const float* lobe6,
+                     uint64_t* states, float* dir, uint8_t* tag, void* stream);
+
+/* lobe_from_stats on n rows of float64 stats (n x 8): mu (n x 2),
+ * cov (n x 4 row-major 2x2), chol (n x 4), trunc_z (n), reset flag (n, may be NULL). */
+int pgg_lobe(int64_t n, const double* stats, double* mu, double* cov, double* chol, double* trunc_z,
+             uint8_t* reset, void* stream);
+
+/* truncation_mass(mu (n x 2), cov (n x 4)) -> z (n). */
+int pgg_trunc_mass(int64_t n, const double* mu, const double* cov, double* z, void* stream);
+
+/* m_step_update(stats (n x 8), sq (n x c x 2), weight, resp (n x c),
+ * valid (n x c u8 or NULL), k_max) -> out (n x 8), all float64. */
+int pgg_m_step(int64_t n, int32_t c, const double* stats, const double* sq, const double* weight,
+               const double* resp, const uint8_t* valid, int32_t k_max, double* out, void* stream);
+
+/* Host function: the (seed, frame, stream_id) prefix of rng.make_streams. */
+uint64_t pgg_frame_key(uint64_t seed, uint64_t frame, uint64_t stream_id);
+
+/* make_streams: states[i] = PCG32 lane state of lanes[i] under `key`. */
+int pgg_make_streams(uint64_t key, int64_t n, const uint64_t* lanes, uint64_t* states, void* stream);
+
+/* next_u32: advance every state once (in place), outputs u32. */
+int pgg_next_u32(int64_t n, uint64_t* states, uint32_t* out, void* stream);
+
+/* Pack reference-layout G-buffer fields (float32/uint8/int32 device arrays,
+ * P pixels) into the planes above.  motion/has_history may be NULL. */
+int pgg_pack_gbuffer(int64_t p, const uint8_t* valid, const float* pos, const float* normal,
+                     const float* depth, const int32_t* kind, const float* albedo, const float* rough,
+                     const float* view, const float* motion, const uint8_t* has_history, uint8_t* flags,
+                     float* nd, float* pr, float* va, float* am, void* stream);
+
+/* Pack VplBuffer fields (valid u8, y f32 x3, radiance f32 x3, strategy u8). */
+int pgg_pack_vpl(int64_t p, const uint8_t* valid, const float* y, const float* radiance,
+                 const uint8_t* strategy, float* vy, float* vl, void* stream);
+
+/* Gamma (P x 8 float32, the reference's (H,W,8) layout) <-> planes. */
+int pgg_gamma_split(int64_t p, const float* aos, float* g0, float* g1, void* stream);
+int pgg_gamma_join(int64_t p, const float* g0, const float* g1, float* aos, void* stream);
+/* Fresh Gamma (mixture.init_stats) into the planes. */
+int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream);
+
+const char* pgg_status_string(int status);
+const char* pgg_last_cuda_error(void);
+int pgg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PGG_H_ */

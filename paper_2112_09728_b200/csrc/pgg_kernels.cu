@@ -1,0 +1,399 @@
+// pgg_kernels.cu — sm_100a kernels and the C ABI of libpgg.so (include/pgg.h).
+//
+// Build (see __graft_entry__.build):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17
+//        -shared -Xcompiler -fPIC -I include csrc/pgg_kernels.cu -o libpgg.so
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "pgg.h"
+#include "pgg_math.cuh"
+#include "pgg_pass.cuh"
+
+using namespace pgg;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+int check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s", cudaGetErrorString(e));
+    return PGG_ERR_CUDA;
+  }
+  return PGG_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int BX = 32, BY = 4;
+
+// ---------------------------------------------------------------------------
+// the guiding pass: one thread per pixel of the band
+
+__global__ void __launch_bounds__(BX * BY) k_guiding_pass(const PassArgs A) {
+  const int x = blockIdx.x * BX + threadIdx.x;
+  const int yl = blockIdx.y * BY + threadIdx.y;
+  if (x >= A.cfg.width || yl >= A.cfg.rows) return;
+  pass_pixel(A, x, yl);
+}
+
+// ---------------------------------------------------------------------------
+// per-lane sampling on caller-owned states
+
+__global__ void k_sample_lanes(int64_t n, int world, const float4* __restrict__ normal,
+                               const float4* __restrict__ view, const float* __restrict__ rough,
+                               const uint8_t* __restrict__ glossy, const uint8_t* __restrict__ guided,
+                               const float* __restrict__ pi, const float* __restrict__ lobe6,
+                               uint64_t* __restrict__ states, float4* __restrict__ dir, uint8_t* __restrict__ tag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 vv = view[i];
+  PixelFrame pf;
+  if (world) {
+    const float4 nn = normal[i];
+    pf = make_pixel_frame(v3(nn.x, nn.y, nn.z), v3(vv.x, vv.y, vv.z));
+  } else {
+    pf.fr.t = v3(1.f, 0.f, 0.f);
+    pf.fr.b = v3(0.f, 1.f, 0.f);
+    pf.fr.n = v3(0.f, 0.f, 1.f);
+    pf.wol = v3(vv.x, vv.y, vv.z);
+    pf.co_pos = vv.z > 0.0f;
+  }
+  const float* l = lobe6 + 6 * i;
+  LobeF L;
+  L.mx = l[0];
+  L.my = l[1];
+  L.l11 = l[2];
+  L.l21 = l[3];
+  L.l22 = l[4];
+  L.z = l[5];
+  L.il11 = 1.0f / L.l11;
+  L.il22 = 1.0f / L.l22;
+  L.gnorm = (float)(1.0 / (2.0 * K<double>::pi * (double)L.l11 * (double)L.l22) / (double)L.z * K<double>::inv_2pi);
+  L.pi = pi[i];
+  L.reset = 0;
+  CholD cd;
+  cd.from_floats = 1;
+  cd.l11f = L.l11;
+  cd.l21f = L.l21;
+  cd.l22f = L.l22;
+  uint64_t st = states[i];
+  const bool gd = world ? (guided[i] != 0) : true;
+  const LaneOut o = sample_lane(pf, glossy[i] != 0, rough[i], gd, L, cd, st);
+  states[i] = st;
+  dir[i] = f4(o.wi.x, o.wi.y, o.wi.z, o.pdf);
+  tag[i] = (uint8_t)(o.gauss | (o.valid << 1));
+}
+
+// ---------------------------------------------------------------------------
+// small batch kernels of the API edge
+
+__global__ void k_lobe(int64_t n, const double* __restrict__ st, double* mu, double* cov, double* chol, double* z,
+                       uint8_t* reset) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* s = st + 8 * i;
+  // mixture.py:129-155 on the caller's float64 stats
+  const double mx = s[0], my = s[1];
+  double sxx = radd(rsub(s[2], rmul(mx, mx)), 1e-4);
+  double syy = radd(rsub(s[3], rmul(my, my)), 1e-4);
+  double sxy = rsub(s[4], rmul(mx, my));
+  const double half = rmul(0.5, radd(sxx, syy));
+  const double dd = rsub(sxx, syy);
+  const double q = radd(rmul(0.25, rmul(dd, dd)), rmul(sxy, sxy));
+  const bool bad = rsub(half, sqrt(fmax(q, 0.0))) < 1e-6;
+  if (bad) {
+    sxx = 0.05;
+    syy = 0.05;
+    sxy = 0.0;
+  }
+  const double l11 = sqrt(sxx);
+  const double l21 = sxy / l11;
+  const double l22 = sqrt(fmax(rsub(syy, rmul(l21, l21)), 1e-30));
+  mu[2 * i] = mx;
+  mu[2 * i + 1] = my;
+  cov[4 * i] = sxx;
+  cov[4 * i + 1] = sxy;
+  cov[4 * i + 2] = sxy;
+  cov[4 * i + 3] = syy;
+  chol[4 * i] = l11;
+  chol[4 * i + 1] = 0.0;
+  chol[4 * i + 2] = l21;
+  chol[4 * i + 3] = l22;
+  z[i] = trunc_mass_f((float)mx, (float)my, (float)l11, (float)l21, (float)l22);
+  if (reset) reset[i] = bad ? 1 : 0;
+}
+
+__global__ void k_trunc(int64_t n, const double* __restrict__ mu, const double* __restrict__ cov, double* z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = cov[4 * i], c = cov[4 * i + 1], b = cov[4 * i + 3];
+  const double l11 = sqrt(a);
+  const double l21 = c / l11;
+  const double l22 = sqrt(fmax(rsub(b, rmul(l21, l21)), 1e-30));
+  z[i] = trunc_mass_f((float)mu[2 * i], (float)mu[2 * i + 1], (float)l11, (float)l21, (float)l22);
+}
+
+__global__ void k_m_step(int64_t n, int c, const double* __restrict__ st, const double* __restrict__ sq,
+                         const double* __restrict__ wt, const double* __restrict__ rs,
+                         const uint8_t* __restrict__ valid, int kmax, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // mixture.py:276-321
+  double bw = 0, bwr = 0, m[5] = {0, 0, 0, 0, 0};
+  for (int j = 0; j < c; ++j) {
+    const int64_t r = i * c + j;
+    const double w = wt[r];
+    if (!(isfinite(w) && w >= 0.0) || (valid && !valid[r])) continue;
+    const double wr = w * rs[r];
+    const double x = sq[2 * r], y = sq[2 * r + 1];
+    bw += w;
+    bwr += wr;
+    m[0] += wr * x;
+    m[1] += wr * y;
+    m[2] += wr * (x * x);
+    m[3] += wr * (y * y);
+    m[4] += wr * (x * y);
+  }
+  const double* s = st + 8 * i;
+  double* o = out + 8 * i;
+  for (int k = 0; k < 8; ++k) o[k] = s[k];
+  if (!(bw > 0.0)) return;
+  const double k = s[7];
+  const double eta = fmax(1.0 / (k + 1.0), 1.0 / (double)kmax);
+  const double den = fmax(bwr, 1e-8);
+  for (int q = 0; q < 5; ++q) o[q] = (1.0 - eta) * s[q] + eta * (m[q] / den);
+  o[6] = fmin(fmax((1.0 - eta) * s[6] + eta * (bwr / fmax(bw, 1e-8)), 0.05), 0.95);
+  o[5] = (1.0 - eta) * s[5] + eta * bwr;
+  o[7] = k + 1.0;
+}
+
+__global__ void k_make_streams(uint64_t key, int64_t n, const uint64_t* __restrict__ lanes, uint64_t* states) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) states[i] = pcg_lane(key, lanes[i]);
+}
+
+__global__ void k_next_u32(int64_t n, uint64_t* states, uint32_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t s = states[i];
+  out[i] = pcg_next(s);
+  states[i] = s;
+}
+
+__global__ void k_pack_gbuffer(int64_t p, const uint8_t* __restrict__ valid, const float* __restrict__ pos,
+                               const float* __restrict__ nrm, const float* __restrict__ depth,
+                               const int32_t* __restrict__ kind, const float* __restrict__ alb,
+                               const float* __restrict__ rough, const float* __restrict__ view,
+                               const float* __restrict__ motion, const uint8_t* __restrict__ hist,
+                               uint8_t* flags, float4* nd, float4* pr, float4* va, float4* am) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  const uint8_t v = valid[i] ? 1 : 0;
+  const uint8_t h = (hist && hist[i]) ? 2 : 0;
+  const uint8_t g = (kind[i] == 1) ? 4 : 0;
+  flags[i] = v | h | g;
+  nd[i] = f4(nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2], depth[i]);
+  pr[i] = f4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], rough[i]);
+  va[i] = f4(view[3 * i], view[3 * i + 1], view[3 * i + 2], alb[3 * i]);
+  am[i] = f4(alb[3 * i + 1], alb[3 * i + 2], motion ? motion[2 * i] : 0.f, motion ? motion[2 * i + 1] : 0.f);
+}
+
+__global__ void k_pack_vpl(int64_t p, const uint8_t* __restrict__ valid, const float* __restrict__ y,
+                           const float* __restrict__ rad, const uint8_t* __restrict__ strat, float4* vy,
+                           float4* vl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  const float use = (valid[i] && strat[i] == 0) ? 1.0f : 0.0f;  // mixture.STRATEGY_BRDF
+  vy[i] = f4(y[3 * i], y[3 * i + 1], y[3 * i + 2], use);
+  vl[i] = f4(rad[3 * i], rad[3 * i + 1], rad[3 * i + 2], 0.0f);
+}
+
+__global__ void k_gamma_split(int64_t p, const float4* __restrict__ aos, float4* g0, float4* g1) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  g0[i] = aos[2 * i];
+  g1[i] = aos[2 * i + 1];
+}
+
+__global__ void k_gamma_join(int64_t p, const float4* __restrict__ g0, const float4* __restrict__ g1, float4* aos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  aos[2 * i] = g0[i];
+  aos[2 * i + 1] = g1[i];
+}
+
+__global__ void k_gamma_init(int64_t p, float4* g0, float4* g1) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  float4 a, b;
+  init_gamma(a, b);
+  g0[i] = a;
+  g1[i] = b;
+}
+
+inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+extern "C" {
+
+int pgg_abi_version(void) { return PGG_ABI_VERSION; }
+
+const char* pgg_status_string(int s) {
+  switch (s) {
+    case PGG_OK: return "ok";
+    case PGG_ERR_ARGUMENT: return "invalid argument";
+    case PGG_ERR_CUDA: return "CUDA launch error";
+    case PGG_ERR_UNSUPPORTED: return "unsupported device";
+    default: return "unknown status";
+  }
+}
+
+const char* pgg_last_cuda_error(void) { return g_cuda_err; }
+
+uint64_t pgg_frame_key(uint64_t seed, uint64_t frame, uint64_t stream_id) {
+  uint64_t h = splitmix64(seed);
+  h = splitmix64(h ^ splitmix64(frame));
+  return splitmix64(h ^ splitmix64(stream_id + 0xA02BDBF7BB3C0A7ULL));
+}
+
+int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                     const pgg_gamma_in* gamma_prev, const pgg_vpl* vpl, const pgg_gamma_out* gamma_reproj,
+                     const pgg_gamma_out* gamma_out, const pgg_samples* samples, int32_t* halo_misses,
+                     void* stream) {
+  if (!cfg || !cur || !gamma_prev) return PGG_ERR_ARGUMENT;
+  if (cfg->width <= 0 || cfg->height <= 0 || cfg->rows < 0 || cfg->row0 < 0 || cfg->row0 + cfg->rows > cfg->height)
+    return PGG_ERR_ARGUMENT;
+  if (cfg->rows == 0) return PGG_OK;
+  if (cur->row0 > cfg->row0 || cur->row0 + cur->rows < cfg->row0 + cfg->rows) return PGG_ERR_ARGUMENT;
+  if (!cur->flags || !cur->nd || !cur->pr || !cur->va || !cur->am) return PGG_ERR_ARGUMENT;
+  if (!gamma_prev->g0 || !gamma_prev->g1) return PGG_ERR_ARGUMENT;
+  if (!prev && (gamma_prev->row0 > cfg->row0 || gamma_prev->row0 + gamma_prev->rows < cfg->row0 + cfg->rows))
+    return PGG_ERR_ARGUMENT;
+  if (vpl && (!gamma_out || !vpl->y || !vpl->L || cfg->k_max < 1)) return PGG_ERR_ARGUMENT;
+  if (samples && (!samples->dir || !samples->tag || cfg->spp < 1 || cfg->nee_draws < 0)) return PGG_ERR_ARGUMENT;
+  PassArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cfg = *cfg;
+  A.cur = *cur;
+  if (prev) A.prev = *prev;
+  A.gin = *gamma_prev;
+  if (vpl) A.vpl = *vpl;
+  if (gamma_reproj) A.grep = *gamma_reproj;
+  if (gamma_out) A.gout = *gamma_out;
+  if (samples) A.smp = *samples;
+  A.has_prev = prev != nullptr;
+  A.has_vpl = vpl != nullptr;
+  A.has_grep = gamma_reproj != nullptr && gamma_reproj->g0 && gamma_reproj->g1;
+  A.has_smp = samples != nullptr;
+  A.halo_misses = halo_misses;
+  const dim3 block(BX, BY);
+  const dim3 grid((cfg->width + BX - 1) / BX, (cfg->rows + BY - 1) / BY);
+  k_guiding_pass<<<grid, block, 0, S(stream)>>>(A);
+  return check_launch();
+}
+
+int pgg_sample_lanes(int64_t n, int32_t world, const float* normal, const float* view, const float* rough,
+                     const uint8_t* glossy, const uint8_t* guided, const float* pi, const float* lobe6,
+                     uint64_t* states, float* dir, uint8_t* tag, void* stream) {
+  if (n < 0 || !view || !rough || !glossy || !pi || !lobe6 || !states || !dir || !tag) return PGG_ERR_ARGUMENT;
+  if (world && (!normal || !guided)) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_sample_lanes<<<blocks(n, 128), 128, 0, S(stream)>>>(
+      n, world, reinterpret_cast<const float4*>(normal), reinterpret_cast<const float4*>(view), rough, glossy,
+      guided, pi, lobe6, states, reinterpret_cast<float4*>(dir), tag);
+  return check_launch();
+}
+
+int pgg_lobe(int64_t n, const double* stats, double* mu, double* cov, double* chol, double* trunc_z, uint8_t* reset,
+             void* stream) {
+  if (n < 0 || !stats || !mu || !cov || !chol || !trunc_z) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lobe<<<blocks(n, 128), 128, 0, S(stream)>>>(n, stats, mu, cov, chol, trunc_z, reset);
+  return check_launch();
+}
+
+int pgg_trunc_mass(int64_t n, const double* mu, const double* cov, double* z, void* stream) {
+  if (n < 0 || !mu || !cov || !z) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_trunc<<<blocks(n, 128), 128, 0, S(stream)>>>(n, mu, cov, z);
+  return check_launch();
+}
+
+int pgg_m_step(int64_t n, int32_t c, const double* stats, const double* sq, const double* weight, const double* resp,
+               const uint8_t* valid, int32_t k_max, double* out, void* stream) {
+  if (n < 0 || c < 0 || !stats || !out || k_max < 1) return PGG_ERR_ARGUMENT;
+  if (c > 0 && (!sq || !weight || !resp)) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_m_step<<<blocks(n, 128), 128, 0, S(stream)>>>(n, c, stats, sq, weight, resp, valid, k_max, out);
+  return check_launch();
+}
+
+int pgg_make_streams(uint64_t key, int64_t n, const uint64_t* lanes, uint64_t* states, void* stream) {
+  if (n < 0 || !lanes || !states) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_make_streams<<<blocks(n, 256), 256, 0, S(stream)>>>(key, n, lanes, states);
+  return check_launch();
+}
+
+int pgg_next_u32(int64_t n, uint64_t* states, uint32_t* out, void* stream) {
+  if (n < 0 || !states || !out) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_next_u32<<<blocks(n, 256), 256, 0, S(stream)>>>(n, states, out);
+  return check_launch();
+}
+
+int pgg_pack_gbuffer(int64_t p, const uint8_t* valid, const float* pos, const float* normal, const float* depth,
+                     const int32_t* kind, const float* albedo, const float* rough, const float* view,
+                     const float* motion, const uint8_t* has_history, uint8_t* flags, float* nd, float* pr,
+                     float* va, float* am, void* stream) {
+  if (p < 0 || !valid || !pos || !normal || !depth || !kind || !albedo || !rough || !view || !flags || !nd || !pr ||
+      !va || !am)
+    return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  k_pack_gbuffer<<<blocks(p, 256), 256, 0, S(stream)>>>(
+      p, valid, pos, normal, depth, kind, albedo, rough, view, motion, has_history, flags,
+      reinterpret_cast<float4*>(nd), reinterpret_cast<float4*>(pr), reinterpret_cast<float4*>(va),
+      reinterpret_cast<float4*>(am));
+  return check_launch();
+}
+
+int pgg_pack_vpl(int64_t p, const uint8_t* valid, const float* y, const float* radiance, const uint8_t* strategy,
+                 float* vy, float* vl, void* stream) {
+  if (p < 0 || !valid || !y || !radiance || !strategy || !vy || !vl) return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  k_pack_vpl<<<blocks(p, 256), 256, 0, S(stream)>>>(p, valid, y, radiance, strategy, reinterpret_cast<float4*>(vy),
+                                                    reinterpret_cast<float4*>(vl));
+  return check_launch();
+}
+
+int pgg_gamma_split(int64_t p, const float* aos, float* g0, float* g1, void* stream) {
+  if (p < 0 || !aos || !g0 || !g1) return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  k_gamma_split<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<const float4*>(aos),
+                                                       reinterpret_cast<float4*>(g0), reinterpret_cast<float4*>(g1));
+  return check_launch();
+}
+
+int pgg_gamma_join(int64_t p, const float* g0, const float* g1, float* aos, void* stream) {
+  if (p < 0 || !aos || !g0 || !g1) return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  k_gamma_join<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<const float4*>(g0),
+                                                      reinterpret_cast<const float4*>(g1),
+                                                      reinterpret_cast<float4*>(aos));
+  return check_launch();
+}
+
+int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream) {
+  if (p < 0 || !g0 || !g1) return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  k_gamma_init<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<float4*>(g0), reinterpret_cast<float4*>(g1));
+  return check_launch();
+}
+
+}  // extern "C"

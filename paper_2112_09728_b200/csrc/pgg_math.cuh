@@ -1,0 +1,598 @@
+// pgg_math.cuh — scalar math of the screen-space guiding pass.
+//
+// One source for the device (sm_100a) and for the test-only host build
+// (csrc/pgg_hostcheck.cpp, compiled with g++ -ffp-contract=off).  Every
+// function is templated on the scalar type T: the hot path instantiates it
+// in float, and the few decisions that must agree with the float64 reference
+// exactly (candidate-offset rint, Box-Muller acceptance, rotated-mean
+// hemisphere test, record validity) are re-evaluated in double inside a
+// guard band around the threshold.
+//
+// Reference semantics (file:line under /root/reference/pkg/src/pgtrace):
+//   PCG32 + SplitMix key chain ........ rng.py:10-55
+//   concentric/Lambert map, ONB ....... sgmap.py:21-115
+//   GGX / Lambert eval, pdf, sample ... scene.py:247-380
+//   lobe, truncation mass, pdfs ....... mixture.py:62-190
+#pragma once
+
+#include <stdint.h>
+#include <vector_types.h>
+
+#ifdef __CUDACC__
+#define PGG_HD __host__ __device__ __forceinline__
+#define PGG_MHD __host__ __device__ __forceinline__
+#else
+#include <math.h>
+#define PGG_HD static inline
+#define PGG_MHD inline
+#endif
+
+namespace pgg {
+
+// ---------------------------------------------------------------------------
+// scalar wrappers (float / double overloads, device intrinsics vs libm)
+
+PGG_HD float m_sqrt(float x) { return sqrtf(x); }
+PGG_HD double m_sqrt(double x) { return sqrt(x); }
+PGG_HD float m_rsqrt(float x) {
+#ifdef __CUDA_ARCH__
+  return rsqrtf(x);
+#else
+  return 1.0f / sqrtf(x);
+#endif
+}
+PGG_HD float m_exp(float x) { return expf(x); }
+PGG_HD double m_exp(double x) { return exp(x); }
+PGG_HD float m_log(float x) { return logf(x); }
+PGG_HD double m_log(double x) { return log(x); }
+PGG_HD float m_log1p(float x) { return log1pf(x); }
+PGG_HD double m_log1p(double x) { return log1p(x); }
+PGG_HD float m_atan(float x) { return atanf(x); }
+PGG_HD double m_atan(double x) { return atan(x); }
+PGG_HD float m_abs(float x) { return fabsf(x); }
+PGG_HD double m_abs(double x) { return fabs(x); }
+PGG_HD float m_max(float a, float b) { return fmaxf(a, b); }
+PGG_HD double m_max(double a, double b) { return fmax(a, b); }
+PGG_HD float m_min(float a, float b) { return fminf(a, b); }
+PGG_HD double m_min(double a, double b) { return fmin(a, b); }
+PGG_HD float m_copysign(float a, float b) { return copysignf(a, b); }
+PGG_HD double m_copysign(double a, double b) { return copysign(a, b); }
+PGG_HD float m_rint(float x) { return rintf(x); }
+PGG_HD double m_rint(double x) { return rint(x); }
+PGG_HD float m_clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
+PGG_HD double m_clamp01(double x) { return fmin(fmax(x, 0.0), 1.0); }
+PGG_HD bool m_isfinite(float x) { return isfinite(x); }
+PGG_HD bool m_isfinite(double x) { return isfinite(x); }
+
+// sin/cos of pi*x (exact argument scaling on the device)
+PGG_HD void m_sincospi(float x, float* s, float* c) {
+#ifdef __CUDA_ARCH__
+  sincospif(x, s, c);
+#else
+  const double a = 3.14159265358979323846 * (double)x;
+  *s = (float)sin(a);
+  *c = (float)cos(a);
+#endif
+}
+PGG_HD void m_sincospi(double x, double* s, double* c) {
+#ifdef __CUDA_ARCH__
+  sincospi(x, s, c);
+#else
+  const double a = 3.14159265358979323846 * x;
+  *s = sin(a);
+  *c = cos(a);
+#endif
+}
+
+// standard normal CDF
+PGG_HD float m_ndtr(float x) {
+#ifdef __CUDA_ARCH__
+  return normcdff(x);
+#else
+  return (float)(0.5 * erfc(-(double)x * 0.70710678118654752440));
+#endif
+}
+PGG_HD double m_ndtr(double x) {
+#ifdef __CUDA_ARCH__
+  return normcdf(x);
+#else
+  return 0.5 * erfc(-x * 0.70710678118654752440);
+#endif
+}
+
+// float64 ops that must not be contracted into FMAs (bitwise agreement with
+// NumPy's separately rounded * and +)
+PGG_HD double rmul(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+PGG_HD double radd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+PGG_HD double rsub(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+
+template <class T> struct K {
+  static constexpr T pi = T(3.14159265358979323846);
+  static constexpr T inv_pi = T(0.31830988618379067154);
+  static constexpr T inv_2pi = T(0.15915494309189533577);
+};
+
+// ---------------------------------------------------------------------------
+// PCG32 streams (rng.py:10-55)
+
+constexpr uint64_t PCG_MUL = 6364136223846793005ULL;
+constexpr uint64_t PCG_INC = 1442695040888963407ULL;
+
+PGG_HD uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// lane state = mix(key ^ mix(lane)) after one warm-up LCG step; key is the
+// per-(seed, frame, stream) prefix of the hash chain (rng.py:34-39)
+PGG_HD uint64_t pcg_lane(uint64_t key, uint64_t lane) {
+  return splitmix64(key ^ splitmix64(lane)) * PCG_MUL + PCG_INC;
+}
+
+PGG_HD uint32_t pcg_next(uint64_t& s) {
+  const uint64_t old = s;
+  s = old * PCG_MUL + PCG_INC;
+  const uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+  const uint32_t rot = (uint32_t)(old >> 59);
+  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+}
+
+// n LCG steps collapsed into one affine map s -> mul*s + add
+constexpr uint64_t pcg_jump_mul(unsigned n) {
+  uint64_t m = 1;
+  for (unsigned i = 0; i < n; ++i) m *= PCG_MUL;
+  return m;
+}
+constexpr uint64_t pcg_jump_add(unsigned n) {
+  uint64_t a = 0;
+  for (unsigned i = 0; i < n; ++i) a = a * PCG_MUL + PCG_INC;
+  return a;
+}
+
+PGG_HD float u01f(uint32_t u) { return (float)u * 2.3283064365386963e-10f; }
+PGG_HD double u01d(uint32_t u) { return (double)u * 2.3283064365386963e-10; }
+
+// ---------------------------------------------------------------------------
+// 3-vectors
+
+template <class T> struct V3 {
+  T x, y, z;
+};
+template <class T> PGG_HD V3<T> v3(T x, T y, T z) { return V3<T>{x, y, z}; }
+template <class T> PGG_HD T dot(const V3<T>& a, const V3<T>& b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+template <class T> PGG_HD V3<T> operator+(const V3<T>& a, const V3<T>& b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+template <class T> PGG_HD V3<T> operator-(const V3<T>& a, const V3<T>& b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+template <class T> PGG_HD V3<T> operator*(const V3<T>& a, T s) { return {a.x * s, a.y * s, a.z * s}; }
+template <class T> PGG_HD V3<T> cross(const V3<T>& a, const V3<T>& b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+template <class T> PGG_HD V3<T> unit(const V3<T>& v) {
+  const T n = m_sqrt(dot(v, v));
+  return v * (T(1) / m_max(n, T(1e-30)));
+}
+template <class D, class S> PGG_HD V3<D> cvt(const V3<S>& v) { return {(D)v.x, (D)v.y, (D)v.z}; }
+
+// Branchless revised ONB keyed on sign(n_z) (sgmap.py:85-98)
+template <class T> struct Frame {
+  V3<T> t, b, n;
+  PGG_MHD V3<T> to_local(const V3<T>& v) const { return {dot(v, t), dot(v, b), dot(v, n)}; }
+  PGG_MHD V3<T> to_world(const V3<T>& v) const {
+    return {t.x * v.x + b.x * v.y + n.x * v.z, t.y * v.x + b.y * v.y + n.y * v.z, t.z * v.x + b.z * v.y + n.z * v.z};
+  }
+};
+template <class T> PGG_HD Frame<T> make_frame(const V3<T>& n) {
+  const T s = m_copysign(T(1), n.z);
+  const T a = T(-1) / (s + n.z);
+  const T b = n.x * n.y * a;
+  Frame<T> f;
+  f.t = {T(1) + s * n.x * n.x * a, s * b, -s * n.x};
+  f.b = {b, s + n.y * n.y * a, -n.y};
+  f.n = n;
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// equal-area square <-> hemisphere (sgmap.py:21-77)
+
+// Concentric map + Lambert lift.  phi is carried in units of pi so the
+// device evaluates sincospi without rounding 2*pi*u first.
+template <class T> PGG_HD V3<T> sq_to_dir(T px, T py) {
+  const T a = T(2) * px - T(1);
+  const T b = T(2) * py - T(1);
+  T r, q;
+  if (m_abs(a) > m_abs(b)) {
+    r = a;
+    q = T(0.25) * (b / a);
+  } else if (b != T(0)) {
+    r = b;
+    q = T(0.5) - T(0.25) * (a / b);
+  } else {
+    r = T(0);
+    q = T(0);
+  }
+  T s, c;
+  m_sincospi(q, &s, &c);
+  const T r2 = r * r;
+  const T lift = m_sqrt(m_max(T(2) - r2, T(0)));
+  return {r * c * lift, r * s * lift, T(1) - r2};
+}
+
+// Inverse lift + inverse concentric map, clipped to [0,1]^2.  Callers pass
+// z >= 0 (the reference raises below -1e-9; sgmap.py:72-73).
+template <class T> PGG_HD void dir_to_sq(const V3<T>& v, T& sx, T& sy) {
+  const T s = m_sqrt(m_max(T(1) + v.z, T(1e-30)));
+  const T x = v.x / s;
+  const T y = v.y / s;
+  const T rho = m_sqrt(x * x + y * y);
+  T a, b;
+  if (rho == T(0)) {
+    a = T(0);
+    b = T(0);
+  } else if (m_abs(x) >= m_abs(y)) {
+    a = m_copysign(rho, x);
+    b = m_atan(y / x) * (T(4) * K<T>::inv_pi) * a;
+  } else {
+    b = m_copysign(rho, y);
+    a = m_atan(x / y) * (T(4) * K<T>::inv_pi) * b;
+  }
+  sx = m_clamp01((a + T(1)) * T(0.5));
+  sy = m_clamp01((b + T(1)) * T(0.5));
+}
+
+// ---------------------------------------------------------------------------
+// BRDFs in a local frame (scene.py:247-380).  The reference evaluates GGX in
+// world space as d = cos_h^2 (a^2 - 1) + 1 with cos_h = h . n for a unit h
+// and the stored (float32, not exactly unit) normal n.  At the specular
+// peak d ~ a^2, so float32 must not form 1 - cos_h^2 by subtraction, and the
+// 1 - |n|^2 ~ 1e-7 offset of the stored normal matters at the 1e-5 level.
+// With h_raw in an orthonormal frame about n/|n| (s^2 = h.x^2 + h.y^2,
+// c = h.z, no normalisation needed):
+//   d = (s^2 + c^2 kappa) / (s^2 + c^2),   kappa = 1 - |n|^2 (1 - a^2)
+// which is the reference's d to float32 relative precision (kappa = a^2 for
+// the exactly-unit local normal e_z of the guided lanes).
+
+template <class T> struct Mat {
+  bool glossy;
+  T a2;     // alpha^2, alpha = max(rough^2, 1e-6)
+  T kappa;  // 1 - |n|^2 (1 - a2)
+};
+
+template <class T> PGG_HD T ggx_d(T a2, T kappa, const V3<T>& h) {
+  const T c2 = h.z * h.z;
+  const T s2 = h.x * h.x + h.y * h.y;
+  const T n2 = s2 + c2;
+  const T d = n2 > T(0) ? (s2 + c2 * kappa) / n2 : T(1);
+  return a2 / m_max(K<T>::pi * d * d, T(1e-30));
+}
+template <class T> PGG_HD T ggx_g1(T a2, T c) {
+  return T(2) * c / m_max(c + m_sqrt(a2 + (T(1) - a2) * c * c), T(1e-30));
+}
+
+// solid-angle pdf of brdf_sample (scene.py:287-308), wo.z = cos_o
+template <class T> PGG_HD T brdf_pdf_local(const Mat<T>& m, const V3<T>& wi, const V3<T>& wo) {
+  if (!(wi.z > T(0) && wo.z > T(0))) return T(0);
+  if (!m.glossy) return wi.z * K<T>::inv_pi;
+  return ggx_g1(m.a2, m_abs(wo.z)) * ggx_d(m.a2, m.kappa, wi + wo) / m_max(T(4) * wo.z, T(1e-30));
+}
+
+// uniforms from a raw draw: u, and 1-u computed from the integer so it keeps
+// full relative precision near u -> 1 (float32 path)
+PGG_HD float u01(uint32_t u, float) { return u01f(u); }
+PGG_HD double u01(uint32_t u, double) { return u01d(u); }
+PGG_HD float om_u01(uint32_t u, float) { return (float)(0x100000000ULL - (uint64_t)u) * 2.3283064365386963e-10f; }
+PGG_HD double om_u01(uint32_t u, double) { return 1.0 - u01d(u); }  // exact in float64
+
+// Lambert cosine sample (scene.py:311-316); z = sqrt(1 - u1)
+template <class T> PGG_HD V3<T> sample_cosine(uint32_t a, uint32_t b) {
+  const T r = m_sqrt(u01(a, T()));
+  T s, c;
+  m_sincospi(T(2) * u01(b, T()), &s, &c);
+  return {r * c, r * s, m_sqrt(m_max(om_u01(a, T()), T(0)))};
+}
+
+// Heitz GGX visible-normal sampling (scene.py:319-351).  `ill` reports the
+// rim case 1 - p1^2 - p2^2 ~ 0 where float32 loses the sqrt argument; the
+// caller then re-evaluates in float64.
+template <class T> PGG_HD V3<T> sample_vndf(T alpha, const V3<T>& wo, uint32_t ua, uint32_t ub, bool& ill) {
+  const V3<T> vh = unit(V3<T>{wo.x * alpha, wo.y * alpha, wo.z});
+  const T l2 = vh.x * vh.x + vh.y * vh.y;
+  V3<T> t1;
+  if (l2 > T(1e-18)) {
+    const T inv = T(1) / m_sqrt(l2);
+    t1 = {-vh.y * inv, vh.x * inv, T(0)};
+  } else {
+    t1 = {T(1), T(0), T(0)};
+  }
+  const V3<T> t2 = cross(vh, t1);
+  const T u1 = u01(ua, T());
+  const T r = m_sqrt(u1);
+  T s, c;
+  m_sincospi(T(2) * u01(ub, T()), &s, &c);
+  const T p1 = r * c;
+  const T a1 = om_u01(ua, T()) + u1 * s * s;  // 1 - p1^2 without cancellation
+  const T sm = T(0.5) * (T(1) + vh.z);
+  const T p2 = (T(1) - sm) * m_sqrt(m_max(a1, T(0))) + sm * (r * s);
+  const T q = a1 - p2 * p2;
+  const T p3 = m_sqrt(m_max(q, T(0)));
+  const V3<T> nh = t1 * p1 + t2 * p2 + vh * p3;
+  const V3<T> hv = V3<T>{alpha * nh.x, alpha * nh.y, m_max(nh.z, T(1e-9))};
+  const T hn = m_sqrt(dot(hv, hv));
+  // q carries ~1e-7 absolute float32 error; its effect on h is
+  // ~1e-7 / (2 p3 |hv|): re-evaluate in float64 where that exceeds ~2e-6
+  ill = q < T(1e-3) || p3 * hn < T(0.03);
+  const V3<T> h = hv * (T(1) / m_max(hn, T(1e-30)));
+  const T k = T(2) * dot(wo, h);
+  return h * k - wo;
+}
+
+// local-frame BRDF draw from two raw draws (scene.py:364-374: the same pair
+// feeds both kinds; glossy lanes take the VNDF sample)
+template <class T> PGG_HD V3<T> brdf_sample_local(const Mat<T>& m, T alpha, const V3<T>& wo, uint32_t a, uint32_t b,
+                                                  bool& ill) {
+  ill = false;
+  if (m.glossy) return sample_vndf(alpha, wo, a, b, ill);
+  return sample_cosine<T>(a, b);
+}
+
+// Tangent frame and local view of a pixel: built in float64 and rounded, so
+// small local components (view near the normal, directions near the
+// horizon) keep their relative precision in the float32 math downstream.
+struct PixelFrame {
+  Frame<float> fr;  // orthonormal frame about n/|n|
+  V3<float> wol;    // view in that frame
+  bool co_pos;      // wo . n > 0 (reference float64 sum order, stored n)
+  float om_nn;      // 1 - |n|^2 of the stored normal (kept relative-exact)
+};
+PGG_HD PixelFrame make_pixel_frame(const V3<float>& n, const V3<float>& wo) {
+  const V3<double> nd = cvt<double>(n);
+  const double nn = dot(nd, nd);
+  const V3<double> nh = nd * (1.0 / sqrt(fmax(nn, 1e-300)));
+  const Frame<double> fd = make_frame(nh);
+  const V3<double> wd = cvt<double>(wo);
+  PixelFrame p;
+  p.fr.t = cvt<float>(fd.t);
+  p.fr.b = cvt<float>(fd.b);
+  p.fr.n = cvt<float>(nh);
+  p.wol = cvt<float>(fd.to_local(wd));
+  p.co_pos = radd(radd(rmul(wd.x, nd.x), rmul(wd.y, nd.y)), rmul(wd.z, nd.z)) > 0.0;
+  p.om_nn = (float)(1.0 - nn);
+  return p;
+}
+
+// kappa of a world-frame evaluation about the stored normal
+PGG_HD float kappa_world(float om_nn, float a2) {
+  return (float)((double)om_nn + (double)a2 * (1.0 - (double)om_nn));
+}
+
+// ---------------------------------------------------------------------------
+// Box-Muller (mixture.py:185-190) from raw u32 draws.  float path: ln(u) via
+// log of the integer (u < 1/2) or log1p(-(2^32-u)/2^32) (u >= 1/2) so the
+// radius keeps full relative accuracy at both ends.
+PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
+  float lnu;
+  if (a == 0u) {
+    lnu = -27.631021115928547f;  // log(1e-12), the reference clamp
+  } else if (a < 0x80000000u) {
+    lnu = m_log((float)a) - 22.180709777918249f;  // - 32 ln 2
+  } else {
+    lnu = m_log1p(-(float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f);
+  }
+  const float r = m_sqrt(-2.0f * lnu);
+  float s, c;
+  m_sincospi(2.0f * u01f(b), &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+PGG_HD void box_muller_d(uint32_t a, uint32_t b, double& z0, double& z1) {
+  const double u1 = m_max(u01d(a), 1e-12);
+  const double r = sqrt(-2.0 * log(u1));
+  const double ang = 2.0 * K<double>::pi * u01d(b);
+  z0 = r * cos(ang);
+  z1 = r * sin(ang);
+}
+
+// ---------------------------------------------------------------------------
+// Gaussian lobe (mixture.py:129-155) and its truncation mass (77-126)
+
+struct LobeF {
+  float mx, my;       // mean
+  float l11, l21, l22;
+  float il11, il22;   // reciprocals for the pdf
+  float gnorm;        // 1 / (2 pi l11 l22 Z) / (2 pi): square density -> solid angle
+  float z;            // truncation mass
+  float pi;           // mixing coefficient (Gamma channel 6)
+  int reset;          // covariance was reset to 0.05 I
+};
+
+#define PGG_GL24(X)                                  \
+  X(0.0024063900014893447f, 0.0061706148999943452f)  \
+  X(0.012635722014345263f, 0.01426569431446678f)     \
+  X(0.030862723998633601f, 0.022138719408709706f)    \
+  X(0.056792236497799464f, 0.02964929245771818f)     \
+  X(0.089999007013048526f, 0.036673240705540081f)    \
+  X(0.12993790421072282f, 0.043095080765976602f)     \
+  X(0.17595317403151223f, 0.048809326052056963f)     \
+  X(0.22728926430558022f, 0.053722135057982782f)     \
+  X(0.28310324618697746f, 0.057752834026862758f)     \
+  X(0.3424786601519183f, 0.060835236463901647f)      \
+  X(0.40444056626319186f, 0.062918728173414123f)     \
+  X(0.46797155356869719f, 0.06396909767337601f)      \
+  X(0.53202844643130276f, 0.06396909767337601f)      \
+  X(0.5955594337368082f, 0.062918728173414123f)      \
+  X(0.6575213398480817f, 0.060835236463901647f)      \
+  X(0.71689675381302254f, 0.057752834026862758f)     \
+  X(0.77271073569441984f, 0.053722135057982782f)     \
+  X(0.82404682596848777f, 0.048809326052056963f)     \
+  X(0.87006209578927718f, 0.043095080765976602f)     \
+  X(0.91000099298695147f, 0.036673240705540081f)     \
+  X(0.94320776350220048f, 0.02964929245771818f)      \
+  X(0.96913727600136634f, 0.022138719408709706f)     \
+  X(0.98736427798565474f, 0.01426569431446678f)      \
+  X(0.99759360999851066f, 0.0061706148999943452f)
+
+// Phi(hi) - Phi(lo), hi > lo, evaluated on the side that avoids cancellation
+PGG_HD float ndtr_diff(float hi, float lo) {
+  if (lo >= 0.0f) return m_ndtr(-lo) - m_ndtr(-hi);
+  return m_ndtr(hi) - m_ndtr(lo);
+}
+
+// Inner-CDF saturation state of one edge term on a segment: 0 = Phi ~ 0,
+// 1 = Phi ~ 1, 2 = ramp (evaluate per node).
+PGG_HD int ramp_state(float arg) { return arg >= 6.5f ? 1 : (arg <= -6.5f ? 0 : 2); }
+
+// Sum_i w_i phi(a + L x_i) over the 24-point rule (without the 1/sqrt(2 pi)).
+PGG_HD float gl24_phi(float a, float len) {
+  float acc = 0.0f;
+#define PGG_X(xn, wn)                          \
+  {                                            \
+    const float z = fmaf(len, xn, a);          \
+    acc = fmaf(wn, m_exp(-0.5f * z * z), acc); \
+  }
+  PGG_GL24(PGG_X)
+#undef PGG_X
+  return acc;
+}
+
+// Truncation mass of N(mu, L L^T) on [0,1]^2, the reference's rule: whitened
+// outer variable on [lo1, hi1] (clipped to +-8.5), break points where the
+// inner edge CDFs saturate (+-6.5), 24-point Gauss-Legendre per segment,
+// clamp [1e-4, 1].  Segments whose inner terms are saturated reduce to the
+// Gaussian-weight sum alone; only ramp segments evaluate Phi per node.
+PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
+  const float lo1 = fmaxf((0.0f - mx) / l11, -8.5f);
+  const float hi1 = fmaxf(fminf((1.0f - mx) / l11, 8.5f), lo1);
+  float acc = 0.0f;
+  if (l21 == 0.0f) {
+    const float len = hi1 - lo1;
+    if (len > 0.0f) {
+      const float g = ndtr_diff((1.0f - my) / l22, (0.0f - my) / l22);
+      acc = len * g * gl24_phi(lo1, len);
+    }
+  } else {
+    const float l21s = fabsf(l21) < 1e-30f ? 1e-30f : l21;
+    float e[6];
+    e[0] = fminf(fmaxf(((0.0f - my) + 6.5f * l22) / l21s, lo1), hi1);
+    e[1] = fminf(fmaxf(((0.0f - my) - 6.5f * l22) / l21s, lo1), hi1);
+    e[2] = fminf(fmaxf(((1.0f - my) + 6.5f * l22) / l21s, lo1), hi1);
+    e[3] = fminf(fmaxf(((1.0f - my) - 6.5f * l22) / l21s, lo1), hi1);
+    e[4] = lo1;
+    e[5] = hi1;
+    // sorting network for 6 keys
+#define PGG_CS(i, j)                     \
+  {                                      \
+    const float lo_ = fminf(e[i], e[j]); \
+    const float hi_ = fmaxf(e[i], e[j]); \
+    e[i] = lo_;                          \
+    e[j] = hi_;                          \
+  }
+    PGG_CS(1, 2) PGG_CS(4, 5) PGG_CS(0, 2) PGG_CS(3, 5) PGG_CS(0, 1) PGG_CS(3, 4)
+    PGG_CS(1, 4) PGG_CS(0, 3) PGG_CS(2, 5) PGG_CS(1, 3) PGG_CS(2, 4) PGG_CS(2, 3)
+#undef PGG_CS
+    const float one_m_my = 1.0f - my;
+    const float m_my = 0.0f - my;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const float a = e[s];
+      const float len = e[s + 1] - a;
+      if (!(len > 0.0f)) continue;
+      const float mid = a + 0.5f * len;
+      const int sh = ramp_state((one_m_my - l21 * mid) / l22);
+      const int sl = ramp_state((m_my - l21 * mid) / l22);
+      if (sh != 2 && sl != 2) {
+        if (sh - sl > 0) acc += len * gl24_phi(a, len);  // Phi(hi) - Phi(lo) = 1
+        continue;
+      }
+      float part = 0.0f;
+#define PGG_X(xn, wn)                                    \
+  {                                                      \
+    const float z = fmaf(len, xn, a);                    \
+    const float hi = (one_m_my - l21 * z) / l22;         \
+    const float lo = (m_my - l21 * z) / l22;             \
+    float g;                                             \
+    if (sh == 2 && sl == 2) g = ndtr_diff(hi, lo);       \
+    else if (sh == 2) g = (sl == 0) ? m_ndtr(hi) : 0.0f; \
+    else g = (sh == 1) ? m_ndtr(-lo) : 0.0f;             \
+    part = fmaf(wn * m_exp(-0.5f * z * z), g, part);     \
+  }
+      PGG_GL24(PGG_X)
+#undef PGG_X
+      acc += len * part;
+    }
+  }
+  acc *= 0.39894228040143267794f;  // 1/sqrt(2 pi)
+  return fminf(fmaxf(acc, 1e-4f), 1.0f);
+}
+
+// Lobe from the float32 Gamma moments.  Covariance, ridge, reset test and
+// Cholesky run in float64 with the reference's operation order and no FMA
+// contraction, so the reset branch and Sigma match the reference bitwise;
+// the float32 lobe feeds the per-record math.
+PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy, float pi) {
+  const double mx = mxf, my = myf;
+  double sxx = radd(rsub((double)m2xx, rmul(mx, mx)), 1e-4);
+  double syy = radd(rsub((double)m2yy, rmul(my, my)), 1e-4);
+  double sxy = rsub((double)m2xy, rmul(mx, my));
+  const double half = rmul(0.5, radd(sxx, syy));
+  const double dd = rsub(sxx, syy);
+  const double q = radd(rmul(0.25, rmul(dd, dd)), rmul(sxy, sxy));
+  const double delta = sqrt(fmax(q, 0.0));
+  const bool reset = rsub(half, delta) < 1e-6;
+  if (reset) {
+    sxx = 0.05;
+    syy = 0.05;
+    sxy = 0.0;
+  }
+  const double l11 = sqrt(sxx);
+  const double l21 = sxy / l11;
+  const double l22 = sqrt(fmax(rsub(syy, rmul(l21, l21)), 1e-30));
+  LobeF L;
+  L.mx = mxf;
+  L.my = myf;
+  L.l11 = (float)l11;
+  L.l21 = (float)l21;
+  L.l22 = (float)l22;
+  L.il11 = (float)(1.0 / l11);
+  L.il22 = (float)(1.0 / l22);
+  L.z = trunc_mass_f(L.mx, L.my, L.l11, L.l21, L.l22);
+  L.gnorm = (float)(1.0 / (2.0 * K<double>::pi * l11 * l22) / (double)L.z * K<double>::inv_2pi);
+  L.pi = pi;
+  L.reset = reset ? 1 : 0;
+  return L;
+}
+
+// solid-angle Gaussian density of a square point (gaussian_pdf_square / 2pi)
+PGG_HD float gauss_sr(const LobeF& L, float sx, float sy) {
+  const float z1 = (sx - L.mx) * L.il11;
+  const float z2 = ((sy - L.my) - L.l21 * z1) * L.il22;
+  return m_exp(-0.5f * (z1 * z1 + z2 * z2)) * L.gnorm;
+}
+
+// EM training budget N = floor((1 - min(k,kmax)/kmax)*15 + 5 + 0.5)
+// (mixture.py:324-328), computed in float64 like the reference
+PGG_HD int neighbor_budget(float k, int kmax) {
+  const double kk = fmin((double)k, (double)kmax);
+  const double raw = radd(rmul(rsub(1.0, kk / (double)kmax), 15.0), 5.0);
+  return (int)floor(radd(raw, 0.5));
+}
+
+}  // namespace pgg

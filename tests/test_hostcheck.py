@@ -1,0 +1,157 @@
+"""CPU checks of the DEVICE formulas: the same pgg_pass.cuh/pgg_math.cuh the
+sm_100a kernels compile, built for the host (tests/hostcheck.py), held to
+the reference golden vectors and the oracle with the tolerance policy of
+SURVEY.md section 8a.  No GPU needed."""
+
+import numpy as np
+import pytest
+
+import golden_io as gio
+import hostcheck as hc
+from oracle import pgg_oracle as O
+
+# tolerance policy (single kernel on identical inputs)
+GAMMA_REL_MAX = 1e-4      # every channel, every pixel (abs floor 1e-7)
+DIR_ABS = 1e-5            # sampled directions, per component
+PDF_REL_P9999 = 1e-4
+PDF_REL_MAX = 1e-3
+
+
+def check_samples(o, wi, pdf, strat, valid):
+    np.testing.assert_array_equal(o["strategy"], strat)
+    np.testing.assert_array_equal(o["valid"], valid)
+    assert np.abs(o["wi"] - wi).max() <= DIR_ABS
+    r = gio.rel_err(o["pdf"], pdf)
+    assert np.percentile(r, 99.99) <= PDF_REL_P9999 and r.max() <= PDF_REL_MAX, (np.percentile(r, 99.99), r.max())
+
+
+def check_gamma(got, ref, exact_k=True):
+    r = gio.rel_err(got, ref)
+    assert r.max() <= GAMMA_REL_MAX, r.reshape(-1, 8).max(0)
+    if exact_k:
+        np.testing.assert_array_equal(got[..., 7], ref[..., 7])
+
+
+@pytest.fixture(scope="module")
+def seq():
+    return gio.load("seq_64x48.npz")
+
+
+@pytest.fixture(scope="module")
+def trained():
+    return gio.load("trained_48x40.npz")
+
+
+@pytest.mark.parametrize("f", range(6))
+def test_seq_frame_stages(seq, f):
+    z = seq
+    spp, seed = int(z["spp"]), int(z["seed"])
+    cur = gio.gbuf_raw(z, f"f{f}_")
+    if f > 0:
+        o = hc.run_pass(cur, z[f"f{f}_gamma_in"], seed, f, prev=gio.gbuf_raw(z, f"f{f-1}_"), spp=spp,
+                        want_samples=False)
+        check_gamma(o["gamma_reproj"], z[f"f{f}_gamma_reproj"])
+        assert o["halo_misses"] == 0
+    o = hc.run_pass(cur, z[f"f{f}_gamma_reproj"], seed, f, vpl=gio.vpl_raw(z, f"f{f}_"), spp=spp)
+    check_samples(o, z[f"f{f}_smp_wi"], z[f"f{f}_smp_pdf"], z[f"f{f}_smp_strategy"], z[f"f{f}_smp_valid"])
+    check_gamma(o["gamma_trained"], z[f"f{f}_gamma_trained"])
+
+
+def test_seq_fused_matches_staged(seq):
+    """reproject -> sample -> train fused in one pass == the staged calls."""
+    z, f = seq, 3
+    spp, seed = int(z["spp"]), int(z["seed"])
+    cur, prev = gio.gbuf_raw(z, f"f{f}_"), gio.gbuf_raw(z, f"f{f-1}_")
+    fused = hc.run_pass(cur, z[f"f{f}_gamma_in"], seed, f, prev=prev, vpl=gio.vpl_raw(z, f"f{f}_"), spp=spp)
+    rep = hc.run_pass(cur, z[f"f{f}_gamma_in"], seed, f, prev=prev, spp=spp, want_samples=False)
+    st = hc.run_pass(cur, rep["gamma_reproj"], seed, f, vpl=gio.vpl_raw(z, f"f{f}_"), spp=spp)
+    for k in ("wi", "pdf", "strategy", "valid", "gamma_trained"):
+        np.testing.assert_array_equal(fused[k], st[k])
+
+
+def test_seq_chain_quantiles(seq):
+    """The device chain over 6 frames against the reference's own chain:
+    trajectory tolerance (>= 99.9 % within 1e-4, max 1e-2, k exact)."""
+    z = seq
+    spp, seed = int(z["spp"]), int(z["seed"])
+    gam = z["f0_gamma_in"]
+    prev = None
+    for f in range(6):
+        cur = gio.gbuf_raw(z, f"f{f}_")
+        o = hc.run_pass(cur, gam, seed, f, prev=prev, vpl=gio.vpl_raw(z, f"f{f}_"), spp=spp)
+        gam = o["gamma_trained"]
+        prev = cur
+    r = gio.rel_err(gam, z["f5_gamma_trained"])
+    assert np.mean(r <= 1e-4) >= 0.999 and r.max() <= 1e-2
+    np.testing.assert_array_equal(gam[..., 7], z["f5_gamma_trained"][..., 7])
+
+
+def test_trained_frame(trained):
+    z = trained
+    spp, seed, fr = int(z["spp"]), int(z["seed"]), int(z["frame"])
+    cur, prev, v = gio.gbuf_raw(z, "c_"), gio.gbuf_raw(z, "p_"), gio.vpl_raw(z, "c_")
+    o = hc.run_pass(cur, z["gamma_in"], seed, fr, prev=prev, spp=spp, want_samples=False)
+    check_gamma(o["gamma_reproj"], z["gamma_reproj"])
+    o = hc.run_pass(cur, z["gamma_in"], seed, fr, vpl=v, spp=spp)
+    check_samples(o, z["smp_wi"], z["smp_pdf"], z["smp_strategy"], z["smp_valid"])
+    check_gamma(o["gamma_trained"], z["gamma_trained"])
+    o = hc.run_pass(cur, z["gamma_in"], seed, fr, vpl=v, spp=spp, k_max=32, radius=7.3, want_samples=False)
+    check_gamma(o["gamma_trained"], z["gamma_trained_r7"])
+
+
+def test_lobe_trunc_mass():
+    z = gio.load("kat.npz")
+    st = z["lobe_stats"]
+    out = np.zeros((st.shape[0], 10), np.float32)
+    hc.lib().pgghc_lobe_f(st.shape[0], hc.P(np.ascontiguousarray(st)), hc.P(out))
+    lb = O.lobe(st.astype(np.float64))
+    np.testing.assert_array_equal(out[:, 7].astype(bool), lb.reset)
+    np.testing.assert_allclose(out[:, 2], lb.l11, rtol=1e-7)
+    np.testing.assert_allclose(out[:, 4], lb.l22, rtol=1e-7)
+    np.testing.assert_allclose(out[:, 3], lb.l21, rtol=1e-7, atol=1e-30)
+    r = gio.rel_err(out[:, 5], z["lobe_z"])
+    assert r.max() <= 2e-5, r.max()       # the reference's own rule error is 2.5e-5
+    assert np.median(r) <= 1e-6
+
+
+def test_disk_offsets_exact():
+    """rint candidate offsets (guard band + float64 recheck) == reference."""
+    st = O.seed_lanes(7, 11, np.arange(200000), 1)
+    a = O.draw_u32(st)
+    b = O.draw_u32(st)
+    out = np.zeros((a.size, 2), np.int32)
+    hc.lib().pgghc_disk_offset(a.size, hc.P(a), hc.P(b), 10.0, hc.P(out))
+    r = 10.0 * np.sqrt(a * 2.0 ** -32)
+    ang = 2.0 * np.pi * (b * 2.0 ** -32)
+    np.testing.assert_array_equal(out[:, 0], np.rint(r * np.cos(ang)))
+    np.testing.assert_array_equal(out[:, 1], np.rint(r * np.sin(ang)))
+
+
+def test_box_muller_accuracy():
+    st = O.seed_lanes(1, 2, np.arange(100000), 0)
+    a = O.draw_u32(st)
+    b = O.draw_u32(st)
+    a[:4] = [0, 1, 0xFFFFFFFF, 0x80000000]
+    z = np.zeros((a.size, 2), np.float32)
+    hc.lib().pgghc_box_muller(a.size, hc.P(a), hc.P(b), hc.P(z))
+    r0, r1 = O.box_muller(a * 2.0 ** -32, b * 2.0 ** -32)
+    assert np.abs(z[:, 0] - r0).max() < 5e-6 and np.abs(z[:, 1] - r1).max() < 5e-6
+
+
+def test_neighbor_budget_exact():
+    k = np.arange(0, 200, dtype=np.float32)
+    for kmax in (64, 100, 7, 1):
+        out = np.zeros(k.size, np.int32)
+        hc.lib().pgghc_neighbor_budget(k.size, hc.P(k), kmax, hc.P(out))
+        np.testing.assert_array_equal(out, O.budget(k, kmax))
+
+
+def test_sgmap_roundtrip_float():
+    rng = np.random.default_rng(3)
+    sq = rng.uniform(0, 1, (100000, 2)).astype(np.float32)
+    d = np.zeros((sq.shape[0], 3), np.float32)
+    hc.lib().pgghc_sq_to_dir(sq.shape[0], hc.P(sq), hc.P(d))
+    np.testing.assert_allclose(d, O.sq_to_dir(sq.astype(np.float64)), atol=2e-6)
+    back = np.zeros_like(sq)
+    hc.lib().pgghc_dir_to_sq(sq.shape[0], hc.P(d), hc.P(back))
+    assert np.abs(back - sq).max() < 1e-5   # SPEC acceptance 1: round trip < 1e-5
