@@ -124,7 +124,7 @@ __global__ void k_lobe(int64_t n, const double* __restrict__ st, double* mu, dou
   chol[4 * i + 1] = 0.0;
   chol[4 * i + 2] = l21;
   chol[4 * i + 3] = l22;
-  z[i] = trunc_mass_f((float)mx, (float)my, (float)l11, (float)l21, (float)l22);
+  z[i] = trunc_mass_bvn(mx, my, sxx, syy, sxy, (float)l11, (float)l21, (float)l22);
   if (reset) reset[i] = bad ? 1 : 0;
 }
 
@@ -135,7 +135,7 @@ __global__ void k_trunc(int64_t n, const double* __restrict__ mu, const double* 
   const double l11 = sqrt(a);
   const double l21 = c / l11;
   const double l22 = sqrt(fmax(rsub(b, rmul(l21, l21)), 1e-30));
-  z[i] = trunc_mass_f((float)mu[2 * i], (float)mu[2 * i + 1], (float)l11, (float)l21, (float)l22);
+  z[i] = trunc_mass_bvn(mu[2 * i], mu[2 * i + 1], a, b, c, (float)l11, (float)l21, (float)l22);
 }
 
 __global__ void k_m_step(int64_t n, int c, const double* __restrict__ st, const double* __restrict__ sq,

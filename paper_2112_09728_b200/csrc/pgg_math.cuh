@@ -543,6 +543,120 @@ PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
   return fminf(fmaxf(acc, 1e-4f), 1.0f);
 }
 
+#define PGG_GLN4(X) \
+  X(0.069431844202973714f, 0.34785484513745357f) \
+  X(0.33000947820757187f, 0.65214515486254643f) \
+  X(0.66999052179242813f, 0.65214515486254643f) \
+  X(0.93056815579702623f, 0.34785484513745357f)
+
+#define PGG_GLN6(X) \
+  X(0.03376524289842403f, 0.17132449237917027f) \
+  X(0.16939530676686776f, 0.36076157304813872f) \
+  X(0.38069040695840156f, 0.46791393457269104f) \
+  X(0.61930959304159849f, 0.46791393457269104f) \
+  X(0.83060469323313224f, 0.36076157304813872f) \
+  X(0.96623475710157591f, 0.17132449237917027f)
+
+#define PGG_GLN10(X) \
+  X(0.013046735741414128f, 0.066671344308688138f) \
+  X(0.067468316655507732f, 0.14945134915058039f) \
+  X(0.16029521585048778f, 0.21908636251598201f) \
+  X(0.28330230293537639f, 0.26926671930999652f) \
+  X(0.42556283050918442f, 0.29552422471475281f) \
+  X(0.57443716949081558f, 0.29552422471475281f) \
+  X(0.71669769706462361f, 0.26926671930999652f) \
+  X(0.83970478414951222f, 0.21908636251598201f) \
+  X(0.93253168334449232f, 0.14945134915058039f) \
+  X(0.98695326425858587f, 0.066671344308688138f)
+
+#define PGG_GLN12(X) \
+  X(0.0092196828766403782f, 0.047175336386511411f) \
+  X(0.047941371814762601f, 0.10693932599531907f) \
+  X(0.11504866290284765f, 0.16007832854334642f) \
+  X(0.20634102285669126f, 0.20316742672306573f) \
+  X(0.31608425050090994f, 0.23349253653835461f) \
+  X(0.43738329574426554f, 0.24914704581340269f) \
+  X(0.5626167042557344f, 0.24914704581340269f) \
+  X(0.68391574949909006f, 0.23349253653835461f) \
+  X(0.79365897714330869f, 0.20316742672306573f) \
+  X(0.88495133709715235f, 0.16007832854334642f) \
+  X(0.95205862818523745f, 0.10693932599531907f) \
+  X(0.99078031712335957f, 0.047175336386511411f)
+
+#define PGG_GLN16(X) \
+  X(0.0052995325041750307f, 0.027152459411754176f) \
+  X(0.0277124884633837f, 0.062253523938647456f) \
+  X(0.067184398806084122f, 0.095158511682492605f) \
+  X(0.1222977958224985f, 0.12462897125553407f) \
+  X(0.19106187779867811f, 0.14959598881657671f) \
+  X(0.27099161117138632f, 0.16915651939500265f) \
+  X(0.35919822461037054f, 0.18260341504492364f) \
+  X(0.45249374508118129f, 0.18945061045506864f) \
+  X(0.54750625491881877f, 0.18945061045506864f) \
+  X(0.64080177538962946f, 0.18260341504492364f) \
+  X(0.72900838882861363f, 0.16915651939500265f) \
+  X(0.80893812220132189f, 0.14959598881657671f) \
+  X(0.87770220417750155f, 0.12462897125553407f) \
+  X(0.93281560119391593f, 0.095158511682492605f) \
+  X(0.9722875115366163f, 0.062253523938647456f) \
+  X(0.99470046749582497f, 0.027152459411754176f)
+
+// Truncation mass as an exact bivariate-normal rectangle probability
+// (Genz 2004, "Numerical computation of rectangular bivariate and trivariate
+// normal probabilities", the |r| < 0.925 Gauss-Legendre form, here used up
+// to |r| < 0.99 with a node count chosen for float32 accuracy):
+//   Z = dPhi_x dPhi_y + asin(r)/(4 pi) sum_i w_i sum_corners +-
+//       exp((sin(asin(r) u_i) h k - (h^2+k^2)/2) / cos^2(asin(r) u_i))
+// over the four standardized corners of [0,1]^2.  It equals the
+// reference's piecewise 24-point rule (mixture.py:84-126) up to that rule's
+// own quadrature error (<= 2.5e-5 relative on extreme lobes, ~1e-15
+// typically); |r| >= 0.99 falls back to the reference rule itself.
+PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double sxy, float l11, float l21,
+                            float l22) {
+  const double sx = sqrt(sxx), sy = sqrt(syy);
+  const double rd = sxy / (sx * sy);
+  const float ar = (float)fabs(rd);
+  float z;
+  if (ar >= 0.99f) {
+    z = trunc_mass_f((float)mx, (float)my, l11, l21, l22);
+  } else {
+    const float a1 = (float)((0.0 - mx) / sx), b1 = (float)((1.0 - mx) / sx);
+    const float a2 = (float)((0.0 - my) / sy), b2 = (float)((1.0 - my) / sy);
+    z = ndtr_diff(b1, a1) * ndtr_diff(b2, a2);
+    if (rd != 0.0) {
+      const float r = (float)rd;
+      const float asr = asinf(r);
+      const float hk0 = a1 * a2, hs0 = 0.5f * (a1 * a1 + a2 * a2);
+      const float hk1 = b1 * a2, hs1 = 0.5f * (b1 * b1 + a2 * a2);
+      const float hk2 = a1 * b2, hs2 = 0.5f * (a1 * a1 + b2 * b2);
+      const float hk3 = b1 * b2, hs3 = 0.5f * (b1 * b1 + b2 * b2);
+      float acc = 0.0f;
+#define PGG_X(un, wn)                                                                       \
+  {                                                                                         \
+    const float sn = sinf(asr * (un));                                                      \
+    const float inv = 1.0f / (1.0f - sn * sn);                                              \
+    const float e = m_exp((sn * hk0 - hs0) * inv) - m_exp((sn * hk1 - hs1) * inv) -          \
+                    m_exp((sn * hk2 - hs2) * inv) + m_exp((sn * hk3 - hs3) * inv);           \
+    acc = fmaf(wn, e, acc);                                                                 \
+  }
+      if (ar < 0.3f) {
+        PGG_GLN4(PGG_X)
+      } else if (ar < 0.75f) {
+        PGG_GLN6(PGG_X)
+      } else if (ar < 0.925f) {
+        PGG_GLN10(PGG_X)
+      } else if (ar < 0.96f) {
+        PGG_GLN12(PGG_X)
+      } else {
+        PGG_GLN16(PGG_X)
+      }
+#undef PGG_X
+      z += acc * asr * 0.079577471545947667884f;  // 1/(4 pi)
+    }
+  }
+  return fminf(fmaxf(z, 1e-4f), 1.0f);
+}
+
 // Lobe from the float32 Gamma moments.  Covariance, ridge, reset test and
 // Cholesky run in float64 with the reference's operation order and no FMA
 // contraction, so the reset branch and Sigma match the reference bitwise;
@@ -573,7 +687,7 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
   L.l22 = (float)l22;
   L.il11 = (float)(1.0 / l11);
   L.il22 = (float)(1.0 / l22);
-  L.z = trunc_mass_f(L.mx, L.my, L.l11, L.l21, L.l22);
+  L.z = trunc_mass_bvn(mx, my, sxx, syy, sxy, L.l11, L.l21, L.l22);
   L.gnorm = (float)(1.0 / (2.0 * K<double>::pi * l11 * l22) / (double)L.z * K<double>::inv_2pi);
   L.pi = pi;
   L.reset = reset ? 1 : 0;

@@ -105,6 +105,11 @@ PGG_HD void lobe_chol_d(float mxf, float myf, float m2xx, float m2yy, float m2xy
 // ---------------------------------------------------------------------------
 // reprojection of one pixel (guide_buffers.py:78-137)
 
+// Mean rotation between the previous and current tangent frames
+// (guide_buffers.py:117-133), in float64: M2 is carried unrotated, so the
+// covariance M2 - mu mu^T of the next lobe cancels and amplifies any error
+// in the rotated mean ~1/Sigma-fold; float64 keeps the float32-rounded mean
+// identical to the reference's in all but boundary-rounding cases.
 PGG_HD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float mux, float muy, bool& keep,
                              float& ox, float& oy) {
   keep = true;
@@ -115,29 +120,16 @@ PGG_HD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float mu
   if (np_.x == nc.x && np_.y == nc.y && np_.z == nc.z && mux >= 1e-6f && mux <= 1.0f - 1e-6f &&
       muy >= 1e-6f && muy <= 1.0f - 1e-6f)
     return;
-  const V3<float> dl = sq_to_dir<float>(mux, muy);
-  const V3<float> dc = make_frame(nc).to_local(make_frame(np_).to_world(dl));
-  if (fabsf(dc.z) < 1e-5f) {
-    // hemisphere test near z = 0: decide in float64
-    const V3<double> dld = sq_to_dir<double>((double)mux, (double)muy);
-    V3<double> dcd =
-        make_frame(cvt<double>(nc)).to_local(make_frame(cvt<double>(np_)).to_world(dld));
-    if (dcd.z < 0.0) {
-      keep = false;
-      return;
-    }
-    double sx, sy;
-    dcd.z = m_max(dcd.z, 0.0);
-    dir_to_sq<double>(dcd, sx, sy);
-    ox = (float)sx;
-    oy = (float)sy;
-    return;
-  }
-  if (dc.z < 0.0f) {
+  const V3<double> dl = sq_to_dir<double>((double)mux, (double)muy);
+  V3<double> dc = make_frame(cvt<double>(nc)).to_local(make_frame(cvt<double>(np_)).to_world(dl));
+  if (dc.z < 0.0) {
     keep = false;
     return;
   }
-  dir_to_sq<float>(dc, ox, oy);
+  double sx, sy;
+  dir_to_sq<double>(dc, sx, sy);
+  ox = (float)sx;
+  oy = (float)sy;
 }
 
 PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const float4& nd, const float4& pr,

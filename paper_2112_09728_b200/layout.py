@@ -157,9 +157,11 @@ class VplPlanes:
         rows, w = v.shape
         out = cls(torch.empty(rows, w, 4, dtype=F32, device=device), torch.empty(rows, w, 4, dtype=F32, device=device),
                   row0)
-        _lib.check(_lib.lib().pgg_pack_vpl(rows * w, _lib.ptr(v), _lib.ptr(dev(y, F32)), _lib.ptr(dev(radiance, F32)),
-                                           _lib.ptr(dev(strategy, torch.uint8)), _lib.ptr(out.y), _lib.ptr(out.L),
-                                           _lib.stream_ptr(stream)))
+        # keep the converted inputs referenced until the launch is enqueued
+        # (a freed temporary's block could be handed to the next conversion)
+        yy, rr, ss = dev(y, F32), dev(radiance, F32), dev(strategy, torch.uint8)
+        _lib.check(_lib.lib().pgg_pack_vpl(rows * w, _lib.ptr(v), _lib.ptr(yy), _lib.ptr(rr), _lib.ptr(ss),
+                                           _lib.ptr(out.y), _lib.ptr(out.L), _lib.stream_ptr(stream)))
         return out
 
     @classmethod
