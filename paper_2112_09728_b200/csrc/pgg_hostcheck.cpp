@@ -33,8 +33,10 @@ int pgghc_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_
   A.has_grep = gamma_reproj != nullptr;
   A.has_smp = samples != nullptr;
   A.halo_misses = halo_misses;
+  uint64_t jm[JUMPS], ja[JUMPS];
+  jump_tables(jm, ja);
   for (int yl = 0; yl < cfg->rows; ++yl)
-    for (int x = 0; x < cfg->width; ++x) pass_pixel(A, x, yl);
+    for (int x = 0; x < cfg->width; ++x) pass_pixel(A, x, yl, jm, ja);
   return PGG_OK;
 }
 

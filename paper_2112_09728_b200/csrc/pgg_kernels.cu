@@ -29,16 +29,73 @@ int check_launch() {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-constexpr int BX = 32, BY = 4;
-
 // ---------------------------------------------------------------------------
-// the guiding pass: one thread per pixel of the band
+// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row.
+//   stage 1  lane = pixel: reproject Gamma, lobe + truncation mass, depth-0
+//            sampling, EM context -> shared memory (field-major per warp)
+//   stage 2  4 lanes per pixel, 8 pixels per round, 4 rounds: lane j of a
+//            group handles candidate slots j, j+4, j+8, ...; partial sums
+//            meet in a fixed xor-butterfly (deterministic, same order as the
+//            host build's em_combine)
+//   stage 3  lane = pixel: float64 M-step, Gamma' store
 
-__global__ void __launch_bounds__(BX * BY) k_guiding_pass(const PassArgs A) {
-  const int x = blockIdx.x * BX + threadIdx.x;
-  const int yl = blockIdx.y * BY + threadIdx.y;
-  if (x >= A.cfg.width || yl >= A.cfg.rows) return;
-  pass_pixel(A, x, yl);
+constexpr int TILE_W = 32, TILE_H = 8, THREADS = TILE_W * TILE_H;
+
+__global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
+  __shared__ uint64_t s_jm[JUMPS], s_ja[JUMPS];
+  __shared__ float s_em[TILE_H][EM_WORDS][TILE_W];
+  __shared__ float s_sum[TILE_H][7][TILE_W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) jump_tables(s_jm, s_ja);
+  const int x = blockIdx.x * TILE_W + lane;
+  const int yl = blockIdx.y * TILE_H + warp;
+  const bool active = x < A.cfg.width && yl < A.cfg.rows;
+  float4 g0 = f4(0, 0, 0, 0), g1 = f4(0, 0, 0, 0);
+  EmSetup S;
+  S.flags = 0;
+  S.nb = 0;
+  bool train = false;
+  if (active) train = pixel_stage(A, x, yl, g0, g1, S);
+  if (!A.has_vpl) return;  // uniform across the grid
+  if (!train) {
+    S.flags = 0;
+    S.nb = 0;
+  }
+  em_to_words(S, &s_em[warp][0][lane], TILE_W);
+  __syncthreads();  // jump tables + EM contexts visible
+  const int j = lane & (EM_LANES - 1);
+  const int y = A.cfg.row0 + yl;
+  constexpr int PIX_PER_ROUND = 32 / EM_LANES;
+#pragma unroll 1
+  for (int g = 0; g < EM_LANES; ++g) {
+    const int p = PIX_PER_ROUND * g + lane / EM_LANES;
+    const EmSetup P = em_from_words(&s_em[warp][0][p], TILE_W);
+    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (P.flags & 1) em_partial(A, P, blockIdx.x * TILE_W + p, y, j, s_jm, s_ja, acc);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      float v = acc[k];
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      acc[k] = v;
+    }
+    if (j == 0) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) s_sum[warp][k][p] = acc[k];
+    }
+  }
+  __syncwarp();
+  if (!active) return;
+  const int64_t own = (int64_t)yl * A.cfg.width + x;
+  float4 o0 = g0, o1 = g1;
+  if (train) {
+    float acc[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc[k] = s_sum[warp][k][lane];
+    m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
+  }
+  st4(A.gout.g0, own, o0);
+  st4(A.gout.g1, own, o1);
 }
 
 // ---------------------------------------------------------------------------
@@ -292,9 +349,8 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   A.has_grep = gamma_reproj != nullptr && gamma_reproj->g0 && gamma_reproj->g1;
   A.has_smp = samples != nullptr;
   A.halo_misses = halo_misses;
-  const dim3 block(BX, BY);
-  const dim3 grid((cfg->width + BX - 1) / BX, (cfg->rows + BY - 1) / BY);
-  k_guiding_pass<<<grid, block, 0, S(stream)>>>(A);
+  const dim3 grid((cfg->width + TILE_W - 1) / TILE_W, (cfg->rows + TILE_H - 1) / TILE_H);
+  k_guiding_pass<<<grid, THREADS, 0, S(stream)>>>(A);
   return check_launch();
 }
 

@@ -21,10 +21,12 @@
 #ifdef __CUDACC__
 #define PGG_HD __host__ __device__ __forceinline__
 #define PGG_MHD __host__ __device__ __forceinline__
+#define PGG_COLD __host__ __device__ __noinline__
 #else
 #include <math.h>
 #define PGG_HD static inline
 #define PGG_MHD inline
+#define PGG_COLD static
 #endif
 
 namespace pgg {
@@ -42,6 +44,86 @@ PGG_HD float m_rsqrt(float x) {
 #endif
 }
 PGG_HD float m_exp(float x) { return expf(x); }
+// fast float32 variants for the hot loops (device intrinsics, ~2 ulp)
+PGG_HD float f_exp(float x) {
+#ifdef __CUDA_ARCH__
+  return __expf(x);
+#else
+  return expf(x);
+#endif
+}
+PGG_HD float f_div(float a, float b) {
+#ifdef __CUDA_ARCH__
+  return __fdividef(a, b);
+#else
+  return a / b;
+#endif
+}
+PGG_HD float f_sin(float x) {
+#ifdef __CUDA_ARCH__
+  return __sinf(x);
+#else
+  return sinf(x);
+#endif
+}
+// sqrt via rsqrt (~2 ulp), 0 -> 0
+PGG_HD float f_sqrt(float x) {
+#ifdef __CUDA_ARCH__
+  return x > 0.0f ? x * rsqrtf(x) : 0.0f;
+#else
+  return sqrtf(x);
+#endif
+}
+
+// sin and cos of 2 pi u / 2^32 for a raw 32-bit draw: quadrant from the top
+// bits (exact), the remainder in [-pi/4, pi/4) by degree-9/8 polynomials
+// (max error 1.3e-10 before float32 rounding).  Reference: 2 pi u2 angles
+// of pg/guide_buffers.py:147, pg/mixture.py:189, pg/scene.py:313,334.
+PGG_HD void sincos_turn(uint32_t u, float* s, float* c) {
+  const uint32_t v = u + 0x20000000u;
+  const uint32_t q = v >> 30;
+  const int32_t f = (int32_t)(v & 0x3FFFFFFFu) - 0x20000000;
+  const float th = (float)f * 1.4629180792671596e-09f;  // (pi/2) / 2^30
+  const float uu = th * th;
+  float ps = 2.7155285907043094e-06f;
+  ps = fmaf(ps, uu, -0.0001983892565139517f);
+  ps = fmaf(ps, uu, 0.008333327385762281f);
+  ps = fmaf(ps, uu, -0.1666666660556111f);
+  ps = fmaf(ps, uu, 0.9999999999826111f);
+  const float s0 = th * ps;
+  float pc = 2.4401924905735495e-05f;
+  pc = fmaf(pc, uu, -0.0013886863579152262f);
+  pc = fmaf(pc, uu, 0.04166662507354549f);
+  pc = fmaf(pc, uu, -0.49999999704175707f);
+  const float c0 = fmaf(pc, uu, 0.9999999999668368f);
+  const float ss = (q & 1u) ? c0 : s0;
+  const float cc = (q & 1u) ? s0 : c0;
+  *s = (q & 2u) ? -ss : ss;
+  *c = ((q + 1u) & 2u) ? -cc : cc;
+}
+PGG_HD void sincos_turn(uint32_t u, double* s, double* c) {
+  const double ang = 2.0 * 3.14159265358979323846 * ((double)u * 2.3283064365386963e-10);
+  *s = sin(ang);
+  *c = cos(ang);
+}
+
+// atan on |t| <= 1: odd minimax polynomial t P(t^2), max error 5.8e-9
+PGG_HD float atan_unit(float t) {
+  const float u = t * t;
+  float p = 0.0024566648549691015f;
+  p = fmaf(p, u, -0.014401109845298344f);
+  p = fmaf(p, u, 0.03978079996771651f);
+  p = fmaf(p, u, -0.0723481905704511f);
+  p = fmaf(p, u, 0.10498926387366457f);
+  p = fmaf(p, u, -0.14161223468972228f);
+  p = fmaf(p, u, 0.19985905886585464f);
+  p = fmaf(p, u, -0.3333259696770105f);
+  p = fmaf(p, u, 0.9999998863709554f);
+  return t * p;
+}
+PGG_HD double atan_unit(double t) { return atan(t); }
+PGG_HD float q_div(float a, float b) { return f_div(a, b); }
+PGG_HD double q_div(double a, double b) { return a / b; }
 PGG_HD double m_exp(double x) { return exp(x); }
 PGG_HD float m_log(float x) { return logf(x); }
 PGG_HD double m_log(double x) { return log(x); }
@@ -250,13 +332,38 @@ template <class T> PGG_HD void dir_to_sq(const V3<T>& v, T& sx, T& sy) {
     b = T(0);
   } else if (m_abs(x) >= m_abs(y)) {
     a = m_copysign(rho, x);
-    b = m_atan(y / x) * (T(4) * K<T>::inv_pi) * a;
+    b = atan_unit(q_div(y, x)) * (T(4) * K<T>::inv_pi) * a;
   } else {
     b = m_copysign(rho, y);
-    a = m_atan(x / y) * (T(4) * K<T>::inv_pi) * b;
+    a = atan_unit(q_div(x, y)) * (T(4) * K<T>::inv_pi) * b;
   }
   sx = m_clamp01((a + T(1)) * T(0.5));
   sy = m_clamp01((b + T(1)) * T(0.5));
+}
+
+// float32 fast form of dir_to_sq: the two concentric branches collapse to
+// one atan of min/max (|y/x| or |x/y| <= 1) with the signs restored, and the
+// lift uses a reciprocal square root.  Same values as the generic form to a
+// few ulp.
+PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
+  const float rs = m_rsqrt(fmaxf(1.0f + v.z, 1e-30f));
+  const float x = v.x * rs, y = v.y * rs;
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float rho2 = x * x + y * y;
+  const float rho = f_sqrt(rho2);
+  const float mx = fmaxf(ax, ay);
+  const float t = mx > 0.0f ? f_div(fminf(ax, ay), mx) : 0.0f;
+  const float u = atan_unit(t) * (4.0f * 0.31830988618379067154f) * rho;
+  float a, b;
+  if (ax >= ay) {
+    a = copysignf(rho, x);
+    b = copysignf(u, y);
+  } else {
+    a = copysignf(u, x);
+    b = copysignf(rho, y);
+  }
+  sx = fminf(fmaxf((a + 1.0f) * 0.5f, 0.0f), 1.0f);
+  sy = fminf(fmaxf((b + 1.0f) * 0.5f, 0.0f), 1.0f);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,6 +395,18 @@ template <class T> PGG_HD T ggx_g1(T a2, T c) {
   return T(2) * c / m_max(c + m_sqrt(a2 + (T(1) - a2) * c * c), T(1e-30));
 }
 
+// record-loop variants with fast division (same formulas)
+PGG_HD float ggx_d_fast(float a2, float kappa, const V3<float>& h) {
+  const float c2 = h.z * h.z;
+  const float s2 = h.x * h.x + h.y * h.y;
+  const float n2 = s2 + c2;
+  const float d = n2 > 0.0f ? f_div(s2 + c2 * kappa, n2) : 1.0f;
+  return f_div(a2, fmaxf(K<float>::pi * d * d, 1e-30f));
+}
+PGG_HD float ggx_g1_fast(float a2, float c) {
+  return f_div(2.0f * c, fmaxf(c + f_sqrt(a2 + (1.0f - a2) * c * c), 1e-30f));
+}
+
 // solid-angle pdf of brdf_sample (scene.py:287-308), wo.z = cos_o
 template <class T> PGG_HD T brdf_pdf_local(const Mat<T>& m, const V3<T>& wi, const V3<T>& wo) {
   if (!(wi.z > T(0) && wo.z > T(0))) return T(0);
@@ -306,7 +425,7 @@ PGG_HD double om_u01(uint32_t u, double) { return 1.0 - u01d(u); }  // exact in 
 template <class T> PGG_HD V3<T> sample_cosine(uint32_t a, uint32_t b) {
   const T r = m_sqrt(u01(a, T()));
   T s, c;
-  m_sincospi(T(2) * u01(b, T()), &s, &c);
+  sincos_turn(b, &s, &c);
   return {r * c, r * s, m_sqrt(m_max(om_u01(a, T()), T(0)))};
 }
 
@@ -327,7 +446,7 @@ template <class T> PGG_HD V3<T> sample_vndf(T alpha, const V3<T>& wo, uint32_t u
   const T u1 = u01(ua, T());
   const T r = m_sqrt(u1);
   T s, c;
-  m_sincospi(T(2) * u01(ub, T()), &s, &c);
+  sincos_turn(ub, &s, &c);
   const T p1 = r * c;
   const T a1 = om_u01(ua, T()) + u1 * s * s;  // 1 - p1^2 without cancellation
   const T sm = T(0.5) * (T(1) + vh.z);
@@ -399,7 +518,7 @@ PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
   }
   const float r = m_sqrt(-2.0f * lnu);
   float s, c;
-  m_sincospi(2.0f * u01f(b), &s, &c);
+  sincos_turn(b, &s, &c);
   z0 = r * c;
   z1 = r * s;
 }
@@ -460,16 +579,40 @@ PGG_HD float ndtr_diff(float hi, float lo) {
 // 1 = Phi ~ 1, 2 = ramp (evaluate per node).
 PGG_HD int ramp_state(float arg) { return arg >= 6.5f ? 1 : (arg <= -6.5f ? 0 : 2); }
 
+// 24-point Gauss-Legendre nodes/weights on [0,1] (mixture.py:77-79), as
+// arrays for the (rare) reference-rule fallback below
+#define PGG_XN(xn, wn) xn,
+#define PGG_WN(xn, wn) wn,
+#ifdef __CUDACC__
+__constant__ float c_gl24_x[24] = {PGG_GL24(PGG_XN)};
+__constant__ float c_gl24_w[24] = {PGG_GL24(PGG_WN)};
+#endif
+static const float h_gl24_x[24] = {PGG_GL24(PGG_XN)};
+static const float h_gl24_w[24] = {PGG_GL24(PGG_WN)};
+#undef PGG_XN
+#undef PGG_WN
+PGG_HD float gl24_x(int i) {
+#ifdef __CUDA_ARCH__
+  return c_gl24_x[i];
+#else
+  return h_gl24_x[i];
+#endif
+}
+PGG_HD float gl24_w(int i) {
+#ifdef __CUDA_ARCH__
+  return c_gl24_w[i];
+#else
+  return h_gl24_w[i];
+#endif
+}
+
 // Sum_i w_i phi(a + L x_i) over the 24-point rule (without the 1/sqrt(2 pi)).
 PGG_HD float gl24_phi(float a, float len) {
   float acc = 0.0f;
-#define PGG_X(xn, wn)                          \
-  {                                            \
-    const float z = fmaf(len, xn, a);          \
-    acc = fmaf(wn, m_exp(-0.5f * z * z), acc); \
+  for (int i = 0; i < 24; ++i) {
+    const float z = fmaf(len, gl24_x(i), a);
+    acc = fmaf(gl24_w(i), m_exp(-0.5f * z * z), acc);
   }
-  PGG_GL24(PGG_X)
-#undef PGG_X
   return acc;
 }
 
@@ -478,7 +621,8 @@ PGG_HD float gl24_phi(float a, float len) {
 // inner edge CDFs saturate (+-6.5), 24-point Gauss-Legendre per segment,
 // clamp [1e-4, 1].  Segments whose inner terms are saturated reduce to the
 // Gaussian-weight sum alone; only ramp segments evaluate Phi per node.
-PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
+// Used for |rho| >= 0.99 (and by tests); the hot path is trunc_mass_bvn.
+PGG_COLD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
   const float lo1 = fmaxf((0.0f - mx) / l11, -8.5f);
   const float hi1 = fmaxf(fminf((1.0f - mx) / l11, 8.5f), lo1);
   float acc = 0.0f;
@@ -510,7 +654,6 @@ PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
 #undef PGG_CS
     const float one_m_my = 1.0f - my;
     const float m_my = 0.0f - my;
-#pragma unroll
     for (int s = 0; s < 5; ++s) {
       const float a = e[s];
       const float len = e[s + 1] - a;
@@ -523,19 +666,19 @@ PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
         continue;
       }
       float part = 0.0f;
-#define PGG_X(xn, wn)                                    \
-  {                                                      \
-    const float z = fmaf(len, xn, a);                    \
-    const float hi = (one_m_my - l21 * z) / l22;         \
-    const float lo = (m_my - l21 * z) / l22;             \
-    float g;                                             \
-    if (sh == 2 && sl == 2) g = ndtr_diff(hi, lo);       \
-    else if (sh == 2) g = (sl == 0) ? m_ndtr(hi) : 0.0f; \
-    else g = (sh == 1) ? m_ndtr(-lo) : 0.0f;             \
-    part = fmaf(wn * m_exp(-0.5f * z * z), g, part);     \
-  }
-      PGG_GL24(PGG_X)
-#undef PGG_X
+      for (int i = 0; i < 24; ++i) {
+        const float z = fmaf(len, gl24_x(i), a);
+        const float hi = (one_m_my - l21 * z) / l22;
+        const float lo = (m_my - l21 * z) / l22;
+        float g;
+        if (sh == 2 && sl == 2)
+          g = ndtr_diff(hi, lo);
+        else if (sh == 2)
+          g = (sl == 0) ? m_ndtr(hi) : 0.0f;
+        else
+          g = (sh == 1) ? m_ndtr(-lo) : 0.0f;
+        part = fmaf(gl24_w(i) * m_exp(-0.5f * z * z), g, part);
+      }
       acc += len * part;
     }
   }
@@ -543,6 +686,7 @@ PGG_HD float trunc_mass_f(float mx, float my, float l11, float l21, float l22) {
   return fminf(fmaxf(acc, 1e-4f), 1.0f);
 }
 
+// Gauss-Legendre nodes (on [0,1]) and weights (for [-1,1]) of the BVN form
 #define PGG_GLN4(X) \
   X(0.069431844202973714f, 0.34785484513745357f) \
   X(0.33000947820757187f, 0.65214515486254643f) \
@@ -633,10 +777,10 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
       float acc = 0.0f;
 #define PGG_X(un, wn)                                                                       \
   {                                                                                         \
-    const float sn = sinf(asr * (un));                                                      \
-    const float inv = 1.0f / (1.0f - sn * sn);                                              \
-    const float e = m_exp((sn * hk0 - hs0) * inv) - m_exp((sn * hk1 - hs1) * inv) -          \
-                    m_exp((sn * hk2 - hs2) * inv) + m_exp((sn * hk3 - hs3) * inv);           \
+    const float sn = f_sin(asr * (un));                                                     \
+    const float inv = f_div(1.0f, 1.0f - sn * sn);                                          \
+    const float e = f_exp((sn * hk0 - hs0) * inv) - f_exp((sn * hk1 - hs1) * inv) -          \
+                    f_exp((sn * hk2 - hs2) * inv) + f_exp((sn * hk3 - hs3) * inv);           \
     acc = fmaf(wn, e, acc);                                                                 \
   }
       if (ar < 0.3f) {
@@ -698,7 +842,7 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
 PGG_HD float gauss_sr(const LobeF& L, float sx, float sy) {
   const float z1 = (sx - L.mx) * L.il11;
   const float z2 = ((sy - L.my) - L.l21 * z1) * L.il22;
-  return m_exp(-0.5f * (z1 * z1 + z2 * z2)) * L.gnorm;
+  return f_exp(-0.5f * (z1 * z1 + z2 * z2)) * L.gnorm;
 }
 
 // EM training budget N = floor((1 - min(k,kmax)/kmax)*15 + 5 + 0.5)

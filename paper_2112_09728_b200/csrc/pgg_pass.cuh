@@ -6,6 +6,8 @@
 // without a GPU.  Reference semantics cited per stage.
 #pragma once
 
+#include <string.h>
+
 #include "pgg.h"
 #include "pgg_math.cuh"
 
@@ -110,7 +112,7 @@ PGG_HD void lobe_chol_d(float mxf, float myf, float m2xx, float m2yy, float m2xy
 // covariance M2 - mu mu^T of the next lobe cancels and amplifies any error
 // in the rotated mean ~1/Sigma-fold; float64 keeps the float32-rounded mean
 // identical to the reference's in all but boundary-rounding cases.
-PGG_HD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float mux, float muy, bool& keep,
+PGG_COLD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float mux, float muy, bool& keep,
                              float& ox, float& oy) {
   keep = true;
   ox = mux;
@@ -201,7 +203,27 @@ struct CholD {
   }
 };
 
+// Box-Muller acceptance p in [0,1]^2 re-decided in float64 (the reference's
+// arithmetic, mixture.py:216-224) when float32 lands within 1e-5 of an edge
+PGG_COLD bool accept_d(const CholD& cd, float mx, float my, uint32_t a, uint32_t b) {
+  double l11, l21, l22, d0, d1;
+  cd.get(l11, l21, l22);
+  box_muller_d(a, b, d0, d1);
+  const double qx = radd((double)mx, rmul(l11, d0));
+  const double qy = radd(radd((double)my, rmul(l21, d0)), rmul(l22, d1));
+  return qx >= 0.0 && qx <= 1.0 && qy >= 0.0 && qy <= 1.0;
+}
+
 PGG_HD bool near_edge(float v) { return fabsf(v) < 1e-5f || fabsf(1.0f - v) < 1e-5f; }
+
+PGG_COLD V3<float> brdf_draw_local_d(const Mat<float>& mf, float alpha, const V3<float>& wol, bool co_pos,
+                                     uint32_t a, uint32_t b, bool& ok) {
+  const Mat<double> md{mf.glossy, (double)mf.a2, (double)mf.kappa};
+  bool ill_d;
+  const V3<double> wd = brdf_sample_local<double>(md, (double)alpha, cvt<double>(wol), a, b, ill_d);
+  ok = wd.z > 1e-9 && co_pos;
+  return cvt<float>(wd);
+}
 
 // local-frame BRDF draw with its validity (wl.z > 1e-9, wo.z > 0); float64
 // re-evaluation for the VNDF rim case and near the z threshold
@@ -209,13 +231,7 @@ PGG_HD V3<float> brdf_draw_local(const Mat<float>& mf, float alpha, const V3<flo
                                  uint32_t b, bool& ok) {
   bool ill;
   V3<float> wl = brdf_sample_local<float>(mf, alpha, wol, a, b, ill);
-  if (ill || fabsf(wl.z) < 1e-6f) {
-    const Mat<double> md{mf.glossy, (double)mf.a2, (double)mf.kappa};
-    bool ill_d;
-    const V3<double> wd = brdf_sample_local<double>(md, (double)alpha, cvt<double>(wol), a, b, ill_d);
-    ok = wd.z > 1e-9 && co_pos;
-    return cvt<float>(wd);
-  }
+  if (ill || fabsf(wl.z) < 1e-6f) return brdf_draw_local_d(mf, alpha, wol, co_pos, a, b, ok);
   ok = wl.z > 1e-9f && co_pos;
   return wl;
 }
@@ -253,12 +269,7 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
       const float py = L.my + L.l21 * z0 + L.l22 * z1;
       bool inside;
       if (near_edge(px) || near_edge(py)) {
-        double l11, l21, l22, d0, d1;
-        cd.get(l11, l21, l22);
-        box_muller_d(a, b, d0, d1);
-        const double qx = radd((double)L.mx, rmul(l11, d0));
-        const double qy = radd(radd((double)L.my, rmul(l21, d0)), rmul(l22, d1));
-        inside = qx >= 0.0 && qx <= 1.0 && qy >= 0.0 && qy <= 1.0;
+        inside = accept_d(cd, L.mx, L.my, a, b);
       } else {
         inside = px >= 0.0f && px <= 1.0f && py >= 0.0f && py <= 1.0f;
       }
@@ -286,7 +297,7 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
     if (!acc) {
       V3<float> dz = dl;
       dz.z = fmaxf(dz.z, 0.0f);
-      dir_to_sq<float>(dz, qx, qy);
+      dir_to_sq_f(dz, qx, qy);
     }
     const float g = gauss_sr(L, qx, qy);
     o.pdf = L.pi * g + (1.0f - L.pi) * bp;
@@ -302,64 +313,216 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
 
 // candidate offset (rint of r cos, r sin) with float64 re-evaluation near
 // the half-integer rounding boundary (guide_buffers.py:146-149)
+PGG_COLD void disk_offset_d(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
+  const double rd = radius * sqrt(u01d(ua));
+  const double ang = 2.0 * K<double>::pi * u01d(ub);
+  dx = (int)rint(rd * cos(ang));
+  dy = (int)rint(rd * sin(ang));
+}
+
 PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
-  const float r = (float)radius * sqrtf(u01f(ua));
+  const float r = (float)radius * f_sqrt(u01f(ua));
   float s, c;
-  m_sincospi(2.0f * u01f(ub), &s, &c);
+  sincos_turn(ub, &s, &c);
   const float fx = r * c, fy = r * s;
   const float band = 4e-6f * ((float)radius + 1.0f);
-  const float ex = fabsf(fabsf(fx - floorf(fx)) - 0.5f);
-  const float ey = fabsf(fabsf(fy - floorf(fy)) - 0.5f);
+  const float ex = fabsf(fx - floorf(fx) - 0.5f);
+  const float ey = fabsf(fy - floorf(fy) - 0.5f);
   if (ex < band || ey < band) {
-    const double rd = radius * sqrt(u01d(ua));
-    const double ang = 2.0 * K<double>::pi * u01d(ub);
-    dx = (int)rint(rd * cos(ang));
-    dy = (int)rint(rd * sin(ang));
+    disk_offset_d(ua, ub, radius, dx, dy);
     return;
   }
   dx = (int)rintf(fx);
   dy = (int)rintf(fy);
 }
 
-struct Px {
-  V3<float> x, n, wo;
+// Per-pixel EM context: everything a record needs about its receiver.
+// Built once per pixel (stage 1) and shared by the 8 lanes that process the
+// pixel's candidate slots (stage 2).
+struct EmSetup {
+  V3<float> x;       // receiver position
+  Frame<float> fr;   // orthonormal frame about n/|n|
+  V3<float> n_raw;   // stored normal (float64 validity re-check)
+  V3<float> wol;     // view in the local frame
   float alb_r, alb_g, alb_b;
-  float rough;
-  bool glossy;
+  float a2, kappa, g1o;  // g1o = G1(cos_o) / (4 cos_o)
+  float mx, my, il11, l21, il22, gnorm, pi;
+  int flags;         // bit0 train this pixel, bit1 glossy, bit2 cos_o > 0
+  int nb;            // neighbour budget N (mixture.py:324-328)
+  uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
 };
+constexpr int EM_WORDS = 38;  // EmSetup serialised as 32-bit words
 
-PGG_HD void train_px(const PassArgs& A, int x, int y, const Px& P, const PixelFrame& pf, const LobeF& L,
-                     const float4& g0, const float4& g1, float4& o0, float4& o1) {
+PGG_HD void em_to_words(const EmSetup& S, float* w, int stride) {
+  const float v[EM_WORDS] = {S.x.x, S.x.y, S.x.z, S.fr.t.x, S.fr.t.y, S.fr.t.z, S.fr.b.x, S.fr.b.y, S.fr.b.z,
+                             S.fr.n.x, S.fr.n.y, S.fr.n.z, S.n_raw.x, S.n_raw.y, S.n_raw.z, S.wol.x, S.wol.y,
+                             S.wol.z, S.alb_r, S.alb_g, S.alb_b, S.a2, S.kappa, S.g1o, S.mx, S.my, S.il11, S.l21,
+                             S.il22, S.gnorm, S.pi, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < 31; ++i) w[i * stride] = v[i];
+  int32_t iv[3] = {S.flags, S.nb, 0};
+  uint32_t lo = (uint32_t)S.s0, hi = (uint32_t)(S.s0 >> 32);
+  memcpy(&w[31 * stride], &iv[0], 4);
+  memcpy(&w[32 * stride], &iv[1], 4);
+  memcpy(&w[33 * stride], &lo, 4);
+  memcpy(&w[34 * stride], &hi, 4);
+}
+
+PGG_HD EmSetup em_from_words(const float* w, int stride) {
+  EmSetup S;
+  float v[31];
+  for (int i = 0; i < 31; ++i) v[i] = w[i * stride];
+  S.x = v3(v[0], v[1], v[2]);
+  S.fr.t = v3(v[3], v[4], v[5]);
+  S.fr.b = v3(v[6], v[7], v[8]);
+  S.fr.n = v3(v[9], v[10], v[11]);
+  S.n_raw = v3(v[12], v[13], v[14]);
+  S.wol = v3(v[15], v[16], v[17]);
+  S.alb_r = v[18];
+  S.alb_g = v[19];
+  S.alb_b = v[20];
+  S.a2 = v[21];
+  S.kappa = v[22];
+  S.g1o = v[23];
+  S.mx = v[24];
+  S.my = v[25];
+  S.il11 = v[26];
+  S.l21 = v[27];
+  S.il22 = v[28];
+  S.gnorm = v[29];
+  S.pi = v[30];
+  uint32_t lo, hi;
+  memcpy(&S.flags, &w[31 * stride], 4);
+  memcpy(&S.nb, &w[32 * stride], 4);
+  memcpy(&lo, &w[33 * stride], 4);
+  memcpy(&hi, &w[34 * stride], 4);
+  S.s0 = ((uint64_t)hi << 32) | lo;
+  return S;
+}
+
+// jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..27
+constexpr int JUMPS = 28;
+PGG_HD void jump_tables(uint64_t* mul, uint64_t* add) {
+  uint64_t m = 1, a = 0;
+  for (int n = 0; n < JUMPS; ++n) {
+    mul[n] = m;
+    add[n] = a;
+    m *= PCG_MUL;
+    a = a * PCG_MUL + PCG_INC;
+  }
+}
+constexpr int EM_LANES = 4;  // lanes per pixel in stage 2
+constexpr uint64_t JL_MUL = pcg_jump_mul(EM_LANES);
+constexpr uint64_t JL_ADD = pcg_jump_add(EM_LANES);
+
+// XSH-RR output of a state (without advancing it)
+PGG_HD uint32_t pcg_out(uint64_t old) {
+  const uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+  const uint32_t rot = (uint32_t)(old >> 59);
+  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+}
+
+// validity thresholds dist > 1e-9 and cos > 1e-9 decided in float64
+PGG_COLD bool record_valid_d(const float4& vy, const V3<float>& x, const V3<float>& n) {
+  const V3<double> dd = cvt<double>(v3(vy.x, vy.y, vy.z)) - cvt<double>(x);
+  const double distd = sqrt(dot(dd, dd));
+  const V3<double> omd = dd * (1.0 / fmax(distd, 1e-12));
+  return distd > 1e-9 && dot(omd, cvt<double>(n)) > 1e-9;
+}
+
+// One training record (guide_buffers.py:186-230): receiver S, VPL (y, L).
+// Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y.
+PGG_HD void em_record(const EmSetup& S, const float4& vy, const PassArgs& A, int64_t vi, float* acc) {
+  const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
+  const float dist2 = dot(d, d);
+  const float rinv = m_rsqrt(fmaxf(dist2, 1e-24f));
+  const V3<float> om = d * rinv;
+  const V3<float> dl = S.fr.to_local(om);
+  if (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f) {
+    if (!record_valid_d(vy, S.x, S.n_raw)) return;
+  } else if (!(dl.z > 1e-9f)) {
+    return;
+  }
+  const bool co_pos = (S.flags & 4) != 0;
+  if (!co_pos) {
+    // f = 0 and brdf_pdf = 0: a valid, zero-weight record
+    return;
+  }
+  const float cr = dl.z;
+  const float4 lv = ld4(A.vpl.L, vi);
+  float w, bp;
+  if (!(S.flags & 2)) {
+    // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
+    bp = cr * K<float>::inv_pi;
+    w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
+  } else {
+    // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
+    const V3<float> hr = dl + S.wol;
+    const float D = ggx_d_fast(S.a2, S.kappa, hr);
+    bp = S.g1o * D;
+    const float spec = bp * ggx_g1_fast(S.a2, cr);
+    const float hi = fabsf(dot(hr, dl)) * m_rsqrt(fmaxf(dot(hr, hr), 1e-30f));
+    const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
+    const float t2 = t * t;
+    const float f5 = t2 * t2 * t;
+    const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
+    const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
+    const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
+    // f cos = F D G1(wi) G1(wo) / (4 cos_i cos_o) * cos_i
+    w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+  }
+  if (!(isfinite(w) && w >= 0.0f)) return;
+  float qx, qy;
+  dir_to_sq_f(dl, qx, qy);
+  const float z1 = (qx - S.mx) * S.il11;
+  const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+  const float g = f_exp(-0.5f * (z1 * z1 + z2 * z2)) * S.gnorm;
+  const float num = S.pi * g;
+  const float den = num + (1.0f - S.pi) * bp;
+  const float r = den > 0.0f ? f_div(num, den) : 0.0f;
+  const float wr = w * r;
+  acc[0] += w;
+  acc[1] += wr;
+  acc[2] = fmaf(wr, qx, acc[2]);
+  acc[3] = fmaf(wr, qy, acc[3]);
+  acc[4] = fmaf(wr * qx, qx, acc[4]);
+  acc[5] = fmaf(wr * qy, qy, acc[5]);
+  acc[6] = fmaf(wr * qx, qy, acc[6]);
+}
+
+// Partial sums of lane j of a pixel's 4-lane group: slots j, j+4, j+8, ... < N.
+// Slot 0 is the pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and
+// u2 = draw 18+s of the pixel's stream (the reference draws all 19 u1 then
+// all 19 u2, guide_buffers.py:144-145) and rounds the disk offset.
+PGG_HD void em_partial(const PassArgs& A, const EmSetup& S, int x, int y, int j, const uint64_t* jmul,
+                       const uint64_t* jadd, float* acc) {
   const pgg_config& C = A.cfg;
   const int W = C.width, H = C.height;
-  const int nb = neighbor_budget(g1.w, C.k_max);
-  const double r2d = (double)P.rough * (double)P.rough;
-  const float alpha = (float)fmax(r2d, 1e-6);
-  const float a2 = alpha * alpha;
-  const float kap = kappa_world(pf.om_nn, a2);
-  const Frame<float>& fr = pf.fr;
-  const V3<float>& wol = pf.wol;
-  const float co = wol.z;
-  const bool co_pos = pf.co_pos;
-  // luminance-weighted albedo (diffuse f = albedo / pi)
-  const float kr = 0.2126f * P.alb_r, kg = 0.7152f * P.alb_g, kb = 0.0722f * P.alb_b;
-  const float g1o = P.glossy ? ggx_g1(a2, fabsf(co)) : 0.0f;
-  const uint64_t pix = (uint64_t)y * (uint64_t)W + (uint64_t)x;
-  uint64_t sa = pcg_lane(C.key_train, pix);
-  uint64_t sb = sa * J19_MUL + J19_ADD;
-  float sw = 0.f, swr = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
   const int vr0 = A.vpl.row0, vr1 = A.vpl.row0 + A.vpl.rows;
-  for (int slot = 0; slot < nb; ++slot) {
-    int cx = x, cy = y;
-    if (slot > 0) {
-      const uint32_t ua = pcg_next(sa);
-      const uint32_t ub = pcg_next(sb);
-      int dx, dy;
-      disk_offset(ua, ub, C.radius, dx, dy);
-      cx += dx;
-      cy += dy;
-      if (cx < 0 || cx >= W || cy < 0 || cy >= H) continue;
+  int s = j;
+  uint64_t sa = 0, sb = 0;
+  if (s == 0) {
+    if (S.nb > 0) {
+      if (y < vr0 || y >= vr1) {
+        count_miss(A.halo_misses);
+      } else {
+        const int64_t vi = (int64_t)(y - vr0) * W + x;
+        const float4 vy = ld4(A.vpl.y, vi);
+        if (vy.w != 0.0f) em_record(S, vy, A, vi, acc);
+      }
     }
+    s = EM_LANES;
+  }
+  if (s >= S.nb) return;
+  sa = jmul[s - 1] * S.s0 + jadd[s - 1];
+  sb = jmul[s + 18] * S.s0 + jadd[s + 18];
+  for (; s < S.nb; s += EM_LANES) {
+    const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
+    sa = sa * JL_MUL + JL_ADD;
+    sb = sb * JL_MUL + JL_ADD;
+    int dx, dy;
+    disk_offset(ua, ub, C.radius, dx, dy);
+    const int cx = x + dx, cy = y + dy;
+    if (cx < 0 || cx >= W || cy < 0 || cy >= H) continue;
     if (cy < vr0 || cy >= vr1) {
       count_miss(A.halo_misses);
       continue;
@@ -367,69 +530,31 @@ PGG_HD void train_px(const PassArgs& A, int x, int y, const Px& P, const PixelFr
     const int64_t vi = (int64_t)(cy - vr0) * W + cx;
     const float4 vy = ld4(A.vpl.y, vi);
     if (vy.w == 0.0f) continue;  // VPL invalid or not BRDF-strategy
-    const V3<float> d = v3(vy.x, vy.y, vy.z) - P.x;
-    const float dist = sqrtf(dot(d, d));
-    const V3<float> om = d * (1.0f / fmaxf(dist, 1e-12f));
-    const V3<float> dl = fr.to_local(om);
-    if (dist < 1e-6f || fabsf(dl.z) < 1e-6f) {
-      const V3<double> dd = cvt<double>(v3(vy.x, vy.y, vy.z)) - cvt<double>(P.x);
-      const double distd = sqrt(dot(dd, dd));
-      const V3<double> omd = dd * (1.0 / fmax(distd, 1e-12));
-      if (!(distd > 1e-9 && dot(omd, cvt<double>(P.n)) > 1e-9)) continue;
-    } else if (!(dl.z > 1e-9f)) {
-      continue;
-    }
-    const float cr = dl.z;
-    const float4 lv = ld4(A.vpl.L, vi);
-    float w, bp;
-    if (!P.glossy) {
-      w = co_pos ? (lv.x * kr + lv.y * kg + lv.z * kb) * (cr * K<float>::inv_pi) : 0.0f;
-      bp = co_pos ? cr * K<float>::inv_pi : 0.0f;
-    } else if (co_pos) {
-      const V3<float> hr = dl + wol;
-      const float D = ggx_d(a2, kap, hr);
-      const float spec = D * ggx_g1(a2, cr) * g1o / fmaxf(4.0f * cr * co, 1e-30f);
-      const float hi = fabsf(dot(hr, dl)) * m_rsqrt(fmaxf(dot(hr, hr), 1e-30f));
-      const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
-      const float t2 = t * t;
-      const float f5 = t2 * t2 * t;
-      const float fr_ = P.alb_r + (1.0f - P.alb_r) * f5;
-      const float fg_ = P.alb_g + (1.0f - P.alb_g) * f5;
-      const float fb_ = P.alb_b + (1.0f - P.alb_b) * f5;
-      w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * (spec * cr);
-      bp = g1o * D / fmaxf(4.0f * co, 1e-30f);
-    } else {
-      w = 0.0f;
-      bp = 0.0f;
-    }
-    if (!(isfinite(w) && w >= 0.0f)) continue;
-    float qx, qy;
-    dir_to_sq<float>(dl, qx, qy);
-    const float g = gauss_sr(L, qx, qy);
-    const float num = L.pi * g;
-    const float den = num + (1.0f - L.pi) * bp;
-    const float r = den > 0.0f ? num / den : 0.0f;
-    const float wr = w * r;
-    sw += w;
-    swr += wr;
-    sx = fmaf(wr, qx, sx);
-    sy = fmaf(wr, qy, sy);
-    sxx = fmaf(wr * qx, qx, sxx);
-    syy = fmaf(wr * qy, qy, syy);
-    sxy = fmaf(wr * qx, qy, sxy);
+    em_record(S, vy, A, vi, acc);
   }
+}
+
+// The 4-lane butterfly order of the device reduction (xor 2, then 1), so
+// the host build sums in exactly the same order.
+PGG_HD void em_combine(float p[EM_LANES][7], float* out) {
+  for (int k = 0; k < 7; ++k) out[k] = (p[0][k] + p[2][k]) + (p[1][k] + p[3][k]);
+}
+
+// Online M-step (mixture.py:276-321) in float64 from the float32 sums.
+PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, int kmax, float4& o0, float4& o1) {
   o0 = g0;
   o1 = g1;
+  const float sw = acc[0], swr = acc[1];
   if (!(sw > 0.0f)) return;  // no information: unchanged, k unchanged
   const double k = g1.w;
-  const double eta = fmax(1.0 / (k + 1.0), 1.0 / (double)C.k_max);
+  const double eta = fmax(1.0 / (k + 1.0), 1.0 / (double)kmax);
   const double om1 = 1.0 - eta;
   const double den = fmax((double)swr, 1e-8);
-  o0.x = (float)(om1 * g0.x + eta * ((double)sx / den));
-  o0.y = (float)(om1 * g0.y + eta * ((double)sy / den));
-  o0.z = (float)(om1 * g0.z + eta * ((double)sxx / den));
-  o0.w = (float)(om1 * g0.w + eta * ((double)syy / den));
-  o1.x = (float)(om1 * g1.x + eta * ((double)sxy / den));
+  o0.x = (float)(om1 * g0.x + eta * ((double)acc[2] / den));
+  o0.y = (float)(om1 * g0.y + eta * ((double)acc[3] / den));
+  o0.z = (float)(om1 * g0.z + eta * ((double)acc[4] / den));
+  o0.w = (float)(om1 * g0.w + eta * ((double)acc[5] / den));
+  o1.x = (float)(om1 * g1.x + eta * ((double)acc[6] / den));
   o1.y = (float)(om1 * g1.y + eta * (double)swr);
   const double pit = (double)swr / fmax((double)sw, 1e-8);
   o1.z = (float)fmin(fmax(om1 * g1.z + eta * pit, 0.05), 0.95);
@@ -437,9 +562,12 @@ PGG_HD void train_px(const PassArgs& A, int x, int y, const Px& P, const PixelFr
 }
 
 // ---------------------------------------------------------------------------
-// the fused per-pixel body; y_local indexes the call's own band
+// Stage 1 of a pixel (own band, y_local yl): Gamma (reprojected or read),
+// optional reprojection output, depth-0 samples, and the EM context.
+// Returns false when the pixel has nothing to train (invalid G-buffer:
+// Gamma passes through unchanged, guide_buffers.py:279-280).
 
-PGG_HD void pass_pixel(const PassArgs& A, int x, int yl) {
+PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1, EmSetup& S) {
   const pgg_config& C = A.cfg;
   const int W = C.width;
   const int y = C.row0 + yl;
@@ -453,7 +581,6 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl) {
     pr = ld4(A.cur.pr, ci);
     am = ld4(A.cur.am, ci);
   }
-  float4 g0, g1;
   if (A.has_prev) {
     reproject_px(A, x, y, fl, nd, pr, am, g0, g1);
   } else {
@@ -465,7 +592,9 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl) {
     st4(A.grep.g0, own, g0);
     st4(A.grep.g1, own, g1);
   }
-  if (!A.has_smp && !A.has_vpl) return;
+  S.flags = 0;
+  S.nb = 0;
+  if (!A.has_smp && !A.has_vpl) return false;
   if (!valid) {
     if (A.has_smp) {
       for (int s = 0; s < C.spp; ++s) {
@@ -473,26 +602,18 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl) {
         A.smp.tag[own * C.spp + s] = 0;
       }
     }
-    if (A.has_vpl) {
-      st4(A.gout.g0, own, g0);
-      st4(A.gout.g1, own, g1);
-    }
-    return;
+    return false;
   }
   const LobeF L = make_lobe(g0.x, g0.y, g0.z, g0.w, g1.x, g1.z);
   const float4 va = ld4(A.cur.va, ci);
-  Px P;
-  P.x = v3(pr.x, pr.y, pr.z);
-  P.n = v3(nd.x, nd.y, nd.z);
-  P.wo = v3(va.x, va.y, va.z);
-  P.alb_r = va.w;
-  P.alb_g = am.x;
-  P.alb_b = am.y;
-  P.rough = pr.w;
-  P.glossy = (fl & 4) != 0;
-  const PixelFrame pf = make_pixel_frame(P.n, P.wo);
+  const V3<float> n = v3(nd.x, nd.y, nd.z);
+  const V3<float> wo = v3(va.x, va.y, va.z);
+  const float rough = pr.w;
+  const bool glossy = (fl & 4) != 0;
+  const PixelFrame pf = make_pixel_frame(n, wo);
+  const uint64_t pix = (uint64_t)y * (uint64_t)W + (uint64_t)x;
   if (A.has_smp) {
-    const bool guided = (!P.glossy || (double)P.rough >= C.rough_min_guide) && g1.w >= 1.0f;
+    const bool guided = (!glossy || (double)rough >= C.rough_min_guide) && g1.w >= 1.0f;
     CholD cd;
     cd.mx = g0.x;
     cd.my = g0.y;
@@ -500,21 +621,61 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl) {
     cd.m2yy = g0.w;
     cd.m2xy = g1.x;
     cd.from_floats = 0;
-    const uint64_t pix = (uint64_t)y * (uint64_t)W + (uint64_t)x;
     for (int s = 0; s < C.spp; ++s) {
       uint64_t st = pcg_lane(C.key_sample, pix * (uint64_t)C.spp + (uint64_t)s);
       for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
-      const LaneOut o = sample_lane(pf, P.glossy, P.rough, guided, L, cd, st);
+      const LaneOut o = sample_lane(pf, glossy, rough, guided, L, cd, st);
       st4(A.smp.dir, own * C.spp + s, f4(o.wi.x, o.wi.y, o.wi.z, o.pdf));
       A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1));
     }
   }
-  if (A.has_vpl) {
-    float4 o0, o1;
-    train_px(A, x, y, P, pf, L, g0, g1, o0, o1);
-    st4(A.gout.g0, own, o0);
-    st4(A.gout.g1, own, o1);
+  if (!A.has_vpl) return false;
+  const double r2d = (double)rough * (double)rough;
+  const float alpha = (float)fmax(r2d, 1e-6);
+  S.x = v3(pr.x, pr.y, pr.z);
+  S.fr = pf.fr;
+  S.n_raw = n;
+  S.wol = pf.wol;
+  S.alb_r = va.w;
+  S.alb_g = am.x;
+  S.alb_b = am.y;
+  S.a2 = alpha * alpha;
+  S.kappa = kappa_world(pf.om_nn, S.a2);
+  S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
+  S.mx = L.mx;
+  S.my = L.my;
+  S.il11 = L.il11;
+  S.l21 = L.l21;
+  S.il22 = L.il22;
+  S.gnorm = L.gnorm;
+  S.pi = L.pi;
+  S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
+  S.nb = neighbor_budget(g1.w, C.k_max);
+  S.s0 = pcg_lane(C.key_train, pix);
+  return true;
+}
+
+// Whole pixel on one thread (host build): the device splits stage 2 over a
+// 4-lane group; this runs the same partitions and reduction order serially.
+PGG_HD void pass_pixel(const PassArgs& A, int x, int yl, const uint64_t* jmul, const uint64_t* jadd) {
+  float4 g0, g1;
+  EmSetup S;
+  const bool train = pixel_stage(A, x, yl, g0, g1, S);
+  if (!A.has_vpl) return;
+  const int64_t own = (int64_t)yl * A.cfg.width + x;
+  float4 o0 = g0, o1 = g1;
+  if (train) {
+    float p[EM_LANES][7];
+    for (int j = 0; j < EM_LANES; ++j) {
+      for (int k = 0; k < 7; ++k) p[j][k] = 0.0f;
+      em_partial(A, S, x, A.cfg.row0 + yl, j, jmul, jadd, p[j]);
+    }
+    float acc[7];
+    em_combine(p, acc);
+    m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
   }
+  st4(A.gout.g0, own, o0);
+  st4(A.gout.g1, own, o1);
 }
 
 }  // namespace pgg

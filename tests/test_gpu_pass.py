@@ -119,5 +119,7 @@ def test_1080p_determinism_and_bands(cuda_dev):
         assert torch.equal(c.gamma.g0, a.gamma.g0[r0:r1]) and torch.equal(c.gamma.g1, a.gamma.g1[r0:r1])
         assert torch.equal(c.samples.dir, a.samples.dir[r0:r1])
         assert torch.equal(c.gamma_reproj.g0, a.gamma_reproj.g0[r0:r1])
-    # sanity: the pass trains (k grows) and samples
-    assert (a.gamma.g1[..., 3] > g.g1[..., 3]).float().mean().item() > 0.5
+    # sanity: most valid pixels train (k grows by one over the reprojected k)
+    grew = (a.gamma.g1[..., 3] == a.gamma_reproj.g1[..., 3] + 1).float()
+    valid = (cur.flags & 1).float()
+    assert (grew * valid).sum().item() > 0.8 * valid.sum().item()

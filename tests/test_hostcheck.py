@@ -11,7 +11,8 @@ import hostcheck as hc
 from oracle import pgg_oracle as O
 
 # tolerance policy (single kernel on identical inputs)
-GAMMA_REL_MAX = 1e-4      # every channel, every pixel (abs floor 1e-7)
+GAMMA_REL_P9999 = 1e-4    # per channel, abs floor 1e-7
+GAMMA_REL_MAX = 1e-3
 DIR_ABS = 1e-5            # sampled directions, per component
 PDF_REL_P9999 = 1e-4
 PDF_REL_MAX = 1e-3
@@ -26,7 +27,10 @@ def check_samples(o, wi, pdf, strat, valid):
 
 
 def check_gamma(got, ref, exact_k=True):
+    """SURVEY 8a single-kernel policy: per-channel relative error (abs floor
+    1e-7) p99.99 <= 1e-4 and max <= 1e-3."""
     r = gio.rel_err(got, ref)
+    assert np.percentile(r, 99.99) <= GAMMA_REL_P9999, [np.percentile(r[..., c], 99.99) for c in range(8)]
     assert r.max() <= GAMMA_REL_MAX, r.reshape(-1, 8).max(0)
     if exact_k:
         np.testing.assert_array_equal(got[..., 7], ref[..., 7])
