@@ -42,11 +42,9 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr int TILE_W = 32, TILE_H = 8, THREADS = TILE_W * TILE_H;
 
 __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
-  __shared__ uint64_t s_jm[JUMPS], s_ja[JUMPS];
   __shared__ float s_em[TILE_H][EM_WORDS][TILE_W];
   __shared__ float s_sum[TILE_H][7][TILE_W];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) jump_tables(s_jm, s_ja);
   const int x = blockIdx.x * TILE_W + lane;
   const int yl = blockIdx.y * TILE_H + warp;
   const bool active = x < A.cfg.width && yl < A.cfg.rows;
@@ -62,7 +60,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
     S.nb = 0;
   }
   em_to_words(S, &s_em[warp][0][lane], TILE_W);
-  __syncthreads();  // jump tables + EM contexts visible
+  __syncwarp();  // this warp's EM contexts visible (warps are independent)
   const int j = lane & (EM_LANES - 1);
   const int y = A.cfg.row0 + yl;
   constexpr int PIX_PER_ROUND = 32 / EM_LANES;
@@ -71,7 +69,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
     const int p = PIX_PER_ROUND * g + lane / EM_LANES;
     const EmSetup P = em_from_words(&s_em[warp][0][p], TILE_W);
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (P.flags & 1) em_partial(A, P, blockIdx.x * TILE_W + p, y, j, s_jm, s_ja, acc);
+    if (P.flags & 1) em_partial(A, P, blockIdx.x * TILE_W + p, y, j, c_jmul, c_jadd, acc);
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
       float v = acc[k];

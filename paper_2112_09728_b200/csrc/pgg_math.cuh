@@ -66,6 +66,27 @@ PGG_HD float f_sin(float x) {
   return sinf(x);
 #endif
 }
+// rsqrt and division refined by one Newton step (~1 ulp) for the
+// accuracy-sensitive record mapping (square point -> Gaussian exponent)
+PGG_HD float r_rsqrt(float x) {
+#ifdef __CUDA_ARCH__
+  const float y = rsqrtf(x);
+  const float e = fmaf(-(x * y), y, 1.0f);
+  return fmaf(0.5f * y, e, y);
+#else
+  return 1.0f / sqrtf(x);
+#endif
+}
+PGG_HD float r_div(float a, float b) {
+#ifdef __CUDA_ARCH__
+  const float r = __frcp_rn(b);
+  const float q = a * r;
+  return fmaf(r, fmaf(-b, q, a), q);
+#else
+  return a / b;
+#endif
+}
+
 // sqrt via rsqrt (~2 ulp), 0 -> 0
 PGG_HD float f_sqrt(float x) {
 #ifdef __CUDA_ARCH__
@@ -346,13 +367,13 @@ template <class T> PGG_HD void dir_to_sq(const V3<T>& v, T& sx, T& sy) {
 // lift uses a reciprocal square root.  Same values as the generic form to a
 // few ulp.
 PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
-  const float rs = m_rsqrt(fmaxf(1.0f + v.z, 1e-30f));
+  const float rs = r_rsqrt(fmaxf(1.0f + v.z, 1e-30f));
   const float x = v.x * rs, y = v.y * rs;
   const float ax = fabsf(x), ay = fabsf(y);
   const float rho2 = x * x + y * y;
-  const float rho = f_sqrt(rho2);
+  const float rho = rho2 > 0.0f ? rho2 * r_rsqrt(rho2) : 0.0f;
   const float mx = fmaxf(ax, ay);
-  const float t = mx > 0.0f ? f_div(fminf(ax, ay), mx) : 0.0f;
+  const float t = mx > 0.0f ? r_div(fminf(ax, ay), mx) : 0.0f;
   const float u = atan_unit(t) * (4.0f * 0.31830988618379067154f) * rho;
   float a, b;
   if (ax >= ay) {
@@ -745,23 +766,49 @@ PGG_COLD float trunc_mass_f(float mx, float my, float l11, float l21, float l22)
   X(0.9722875115366163f, 0.062253523938647456f) \
   X(0.99470046749582497f, 0.027152459411754176f)
 
+#define PGG_GLN24(X) \
+  X(0.0024063900014893447f, 0.01234122979998869f) \
+  X(0.012635722014345263f, 0.028531388628933559f) \
+  X(0.030862723998633601f, 0.044277438817419412f) \
+  X(0.056792236497799464f, 0.05929858491543636f) \
+  X(0.089999007013048526f, 0.073346481411080161f) \
+  X(0.12993790421072282f, 0.086190161531953205f) \
+  X(0.17595317403151223f, 0.097618652104113926f) \
+  X(0.22728926430558022f, 0.10744427011596556f) \
+  X(0.28310324618697746f, 0.11550566805372552f) \
+  X(0.3424786601519183f, 0.12167047292780329f) \
+  X(0.40444056626319186f, 0.12583745634682825f) \
+  X(0.46797155356869719f, 0.12793819534675202f) \
+  X(0.53202844643130276f, 0.12793819534675202f) \
+  X(0.5955594337368082f, 0.12583745634682825f) \
+  X(0.6575213398480817f, 0.12167047292780329f) \
+  X(0.71689675381302254f, 0.11550566805372552f) \
+  X(0.77271073569441984f, 0.10744427011596556f) \
+  X(0.82404682596848777f, 0.097618652104113926f) \
+  X(0.87006209578927718f, 0.086190161531953205f) \
+  X(0.91000099298695147f, 0.073346481411080161f) \
+  X(0.94320776350220048f, 0.05929858491543636f) \
+  X(0.96913727600136634f, 0.044277438817419412f) \
+  X(0.98736427798565474f, 0.028531388628933559f) \
+  X(0.99759360999851066f, 0.01234122979998869f)
+
 // Truncation mass as an exact bivariate-normal rectangle probability
 // (Genz 2004, "Numerical computation of rectangular bivariate and trivariate
 // normal probabilities", the |r| < 0.925 Gauss-Legendre form, here used up
-// to |r| < 0.99 with a node count chosen for float32 accuracy):
+// to |r| < 0.999 with a node count chosen for float32 accuracy):
 //   Z = dPhi_x dPhi_y + asin(r)/(4 pi) sum_i w_i sum_corners +-
 //       exp((sin(asin(r) u_i) h k - (h^2+k^2)/2) / cos^2(asin(r) u_i))
 // over the four standardized corners of [0,1]^2.  It equals the
 // reference's piecewise 24-point rule (mixture.py:84-126) up to that rule's
 // own quadrature error (<= 2.5e-5 relative on extreme lobes, ~1e-15
-// typically); |r| >= 0.99 falls back to the reference rule itself.
+// typically); |r| >= 0.999 falls back to the reference rule itself.
 PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double sxy, float l11, float l21,
                             float l22) {
   const double sx = sqrt(sxx), sy = sqrt(syy);
   const double rd = sxy / (sx * sy);
   const float ar = (float)fabs(rd);
   float z;
-  if (ar >= 0.99f) {
+  if (ar >= 0.999f) {
     z = trunc_mass_f((float)mx, (float)my, l11, l21, l22);
   } else {
     const float a1 = (float)((0.0 - mx) / sx), b1 = (float)((1.0 - mx) / sx);
@@ -791,8 +838,10 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
         PGG_GLN10(PGG_X)
       } else if (ar < 0.96f) {
         PGG_GLN12(PGG_X)
-      } else {
+      } else if (ar < 0.99f) {
         PGG_GLN16(PGG_X)
+      } else {
+        PGG_GLN24(PGG_X)
       }
 #undef PGG_X
       z += acc * asr * 0.079577471545947667884f;  // 1/(4 pi)

@@ -401,6 +401,12 @@ PGG_HD EmSetup em_from_words(const float* w, int stride) {
 
 // jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..27
 constexpr int JUMPS = 28;
+#define PGG_J7(F, b) F(b + 0), F(b + 1), F(b + 2), F(b + 3), F(b + 4), F(b + 5), F(b + 6)
+#define PGG_JTAB(F) PGG_J7(F, 0), PGG_J7(F, 7), PGG_J7(F, 14), PGG_J7(F, 21)
+#ifdef __CUDACC__
+__constant__ uint64_t c_jmul[JUMPS] = {PGG_JTAB(pcg_jump_mul)};
+__constant__ uint64_t c_jadd[JUMPS] = {PGG_JTAB(pcg_jump_add)};
+#endif
 PGG_HD void jump_tables(uint64_t* mul, uint64_t* add) {
   uint64_t m = 1, a = 0;
   for (int n = 0; n < JUMPS; ++n) {
@@ -434,7 +440,7 @@ PGG_COLD bool record_valid_d(const float4& vy, const V3<float>& x, const V3<floa
 PGG_HD void em_record(const EmSetup& S, const float4& vy, const PassArgs& A, int64_t vi, float* acc) {
   const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
   const float dist2 = dot(d, d);
-  const float rinv = m_rsqrt(fmaxf(dist2, 1e-24f));
+  const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
   const V3<float> om = d * rinv;
   const V3<float> dl = S.fr.to_local(om);
   if (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f) {
@@ -549,12 +555,12 @@ PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, i
   const double k = g1.w;
   const double eta = fmax(1.0 / (k + 1.0), 1.0 / (double)kmax);
   const double om1 = 1.0 - eta;
-  const double den = fmax((double)swr, 1e-8);
-  o0.x = (float)(om1 * g0.x + eta * ((double)acc[2] / den));
-  o0.y = (float)(om1 * g0.y + eta * ((double)acc[3] / den));
-  o0.z = (float)(om1 * g0.z + eta * ((double)acc[4] / den));
-  o0.w = (float)(om1 * g0.w + eta * ((double)acc[5] / den));
-  o1.x = (float)(om1 * g1.x + eta * ((double)acc[6] / den));
+  const double ed = eta / fmax((double)swr, 1e-8);
+  o0.x = (float)(om1 * g0.x + ed * (double)acc[2]);
+  o0.y = (float)(om1 * g0.y + ed * (double)acc[3]);
+  o0.z = (float)(om1 * g0.z + ed * (double)acc[4]);
+  o0.w = (float)(om1 * g0.w + ed * (double)acc[5]);
+  o1.x = (float)(om1 * g1.x + ed * (double)acc[6]);
   o1.y = (float)(om1 * g1.y + eta * (double)swr);
   const double pit = (double)swr / fmax((double)sw, 1e-8);
   o1.z = (float)fmin(fmax(om1 * g1.z + eta * pit, 0.05), 0.95);
