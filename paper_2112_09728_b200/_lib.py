@@ -12,7 +12,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpgg.so")
+LIB_PATH = os.environ.get("PGG_LIB") or os.path.join(_HERE, "libpgg.so")  # PGG_LIB: A/B builds
 
 
 class PggUnavailable(RuntimeError):

@@ -3,6 +3,7 @@
 // Build (see __graft_entry__.build):
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17
 //        -shared -Xcompiler -fPIC -I include csrc/pgg_kernels.cu -o libpgg.so
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -40,11 +41,90 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 //   stage 3  lane = pixel: float64 M-step, Gamma' store
 
 constexpr int TILE_W = 32, TILE_H = 8, THREADS = TILE_W * TILE_H;
+constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this radius
 
-__global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
-  __shared__ float s_em[TILE_H][EM_WORDS][TILE_W];
-  __shared__ float s_sum[TILE_H][7][TILE_W];
+#ifndef PGG_MIN_BLOCKS
+#define PGG_MIN_BLOCKS 2
+#endif
+
+// shared-memory carve-up of one block
+struct SmemLayout {
+  int R, cols, rows;
+  size_t tile_bytes, off_l, off_em, off_sum, off_bar, total;
+  __host__ __device__ SmemLayout(int r, bool tile) : R(r), cols(TILE_W + 2 * r), rows(TILE_H + 2 * r) {
+    tile_bytes = tile ? (size_t)cols * rows * 16 : 0;
+    off_l = (tile_bytes + 127) & ~(size_t)127;
+    off_em = off_l + ((tile_bytes + 127) & ~(size_t)127);
+    off_sum = off_em + (size_t)TILE_H * EM_WORDS * TILE_W * 4;
+    off_bar = off_sum + (size_t)TILE_H * 7 * TILE_W * 4;
+    total = off_bar + 16;
+  }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// TMA: 2-D tiled bulk copy global -> shared, completion on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row.
+//   stage 0  (kTile) one thread issues two TMA loads of the block's VPL tile
+//            plus the EM halo (Pi y and L planes) into shared memory; they
+//            land while stage 1 runs
+//   stage 1  lane = pixel: reproject Gamma, lobe + truncation mass, depth-0
+//            sampling, EM context -> shared memory (field-major per warp)
+//   stage 2  4 lanes per pixel, 8 pixels per round, 4 rounds: lane j of a
+//            group handles candidate slots j, j+4, j+8, ...; partial sums
+//            meet in a fixed xor-butterfly (deterministic, same order as the
+//            host build's em_combine)
+//   stage 3  lane = pixel: float64 M-step, Gamma' store
+// Warps never wait for each other after the start-up barrier.
+
+template <bool kTile>
+__global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
+    k_guiding_pass(const PassArgs A, const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmL,
+                   int R) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const SmemLayout SL(R, kTile);
+  float4* tile_y = reinterpret_cast<float4*>(smem);
+  float4* tile_l = reinterpret_cast<float4*>(smem + SL.off_l);
+  float* s_em = reinterpret_cast<float*>(smem + SL.off_em);
+  float* s_sum = reinterpret_cast<float*>(smem + SL.off_sum);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SL.off_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int band_y0 = A.cfg.row0 + blockIdx.y * TILE_H;  // frame row of the tile's first row
+  if (kTile && A.has_vpl) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(2 * SL.tile_bytes);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                   : "memory");
+      const int c0 = (int)(blockIdx.x * TILE_W - R) * 4;
+      const int c1 = band_y0 - R - A.vpl.row0;
+      tma_load_2d(tile_y, &tmY, c0, c1, bar);
+      tma_load_2d(tile_l, &tmL, c0, c1, bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+  }
   const int x = blockIdx.x * TILE_W + lane;
   const int yl = blockIdx.y * TILE_H + warp;
   const bool active = x < A.cfg.width && yl < A.cfg.rows;
@@ -59,17 +139,28 @@ __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
     S.flags = 0;
     S.nb = 0;
   }
-  em_to_words(S, &s_em[warp][0][lane], TILE_W);
-  __syncwarp();  // this warp's EM contexts visible (warps are independent)
+  float* my_em = s_em + warp * EM_WORDS * TILE_W;
+  em_to_words(S, my_em + lane, TILE_W);
+  __syncwarp();
+  if (kTile) mbar_wait(bar, 0);
   const int j = lane & (EM_LANES - 1);
   const int y = A.cfg.row0 + yl;
   constexpr int PIX_PER_ROUND = 32 / EM_LANES;
 #pragma unroll 1
   for (int g = 0; g < EM_LANES; ++g) {
     const int p = PIX_PER_ROUND * g + lane / EM_LANES;
-    const EmSetup P = em_from_words(&s_em[warp][0][p], TILE_W);
+    const EmSetup P = em_from_words(my_em + p, TILE_W);
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (P.flags & 1) em_partial(A, P, blockIdx.x * TILE_W + p, y, j, c_jmul, c_jadd, acc);
+    if (P.flags & 1) {
+      const int px = blockIdx.x * TILE_W + p;
+      if (kTile) {
+        const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
+        em_partial(A, V, P, px, y, j, c_jmul, c_jadd, acc);
+      } else {
+        const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
+        em_partial(A, V, P, px, y, j, c_jmul, c_jadd, acc);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
       float v = acc[k];
@@ -79,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
     }
     if (j == 0) {
 #pragma unroll
-      for (int k = 0; k < 7; ++k) s_sum[warp][k][p] = acc[k];
+      for (int k = 0; k < 7; ++k) s_sum[(warp * 7 + k) * TILE_W + p] = acc[k];
     }
   }
   __syncwarp();
@@ -89,11 +180,56 @@ __global__ void __launch_bounds__(THREADS, 2) k_guiding_pass(const PassArgs A) {
   if (train) {
     float acc[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) acc[k] = s_sum[warp][k][lane];
+    for (int k = 0; k < 7; ++k) acc[k] = s_sum[(warp * 7 + k) * TILE_W + lane];
     m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
   }
   st4(A.gout.g0, own, o0);
   st4(A.gout.g1, own, o1);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// VPL plane (rows x W float4) as a 2-D float32 tensor of 4W x rows, box of
+// the tile + halo
+bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int R) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)4 * width, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)4 * width * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)(4 * (TILE_W + 2 * R)), (cuuint32_t)(TILE_H + 2 * R)};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(plane), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool kTile>
+int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
+  const SmemLayout SL(R, kTile);
+  static bool attr_set[MAX_TILE_R + 1] = {};
+  if (SL.total > 48 * 1024 && !attr_set[R]) {
+    cudaFuncSetAttribute(k_guiding_pass<kTile>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
+    attr_set[R] = true;
+  }
+  const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
+  k_guiding_pass<kTile><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
+  return check_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -347,9 +483,15 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   A.has_grep = gamma_reproj != nullptr && gamma_reproj->g0 && gamma_reproj->g1;
   A.has_smp = samples != nullptr;
   A.halo_misses = halo_misses;
-  const dim3 grid((cfg->width + TILE_W - 1) / TILE_W, (cfg->rows + TILE_H - 1) / TILE_H);
-  k_guiding_pass<<<grid, THREADS, 0, S(stream)>>>(A);
-  return check_launch();
+  // stage the VPL neighbourhood through shared memory (TMA) when the halo fits
+  const int R = (int)ceil(cfg->radius > 0.0 ? cfg->radius : 0.0);
+  CUtensorMap my, ml;
+  memset(&my, 0, sizeof(my));
+  memset(&ml, 0, sizeof(ml));
+  if (vpl && R <= MAX_TILE_R && encode_vpl_map(&my, vpl->y, cfg->width, vpl->rows, R) &&
+      encode_vpl_map(&ml, vpl->L, cfg->width, vpl->rows, R))
+    return launch_pass<true>(A, my, ml, R, S(stream));
+  return launch_pass<false>(A, my, ml, 0, S(stream));
 }
 
 int pgg_sample_lanes(int64_t n, int32_t world, const float* normal, const float* view, const float* rough,

@@ -351,16 +351,16 @@ struct EmSetup {
   int nb;            // neighbour budget N (mixture.py:324-328)
   uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
 };
-constexpr int EM_WORDS = 38;  // EmSetup serialised as 32-bit words
+constexpr int EM_WORDS = 35;  // EmSetup serialised as 32-bit words
 
 PGG_HD void em_to_words(const EmSetup& S, float* w, int stride) {
-  const float v[EM_WORDS] = {S.x.x, S.x.y, S.x.z, S.fr.t.x, S.fr.t.y, S.fr.t.z, S.fr.b.x, S.fr.b.y, S.fr.b.z,
-                             S.fr.n.x, S.fr.n.y, S.fr.n.z, S.n_raw.x, S.n_raw.y, S.n_raw.z, S.wol.x, S.wol.y,
-                             S.wol.z, S.alb_r, S.alb_g, S.alb_b, S.a2, S.kappa, S.g1o, S.mx, S.my, S.il11, S.l21,
-                             S.il22, S.gnorm, S.pi, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const float v[31] = {S.x.x, S.x.y, S.x.z, S.fr.t.x, S.fr.t.y, S.fr.t.z, S.fr.b.x, S.fr.b.y, S.fr.b.z,
+                       S.fr.n.x, S.fr.n.y, S.fr.n.z, S.n_raw.x, S.n_raw.y, S.n_raw.z, S.wol.x, S.wol.y,
+                       S.wol.z, S.alb_r, S.alb_g, S.alb_b, S.a2, S.kappa, S.g1o, S.mx, S.my, S.il11, S.l21,
+                       S.il22, S.gnorm, S.pi};
   for (int i = 0; i < 31; ++i) w[i * stride] = v[i];
-  int32_t iv[3] = {S.flags, S.nb, 0};
-  uint32_t lo = (uint32_t)S.s0, hi = (uint32_t)(S.s0 >> 32);
+  const int32_t iv[2] = {S.flags, S.nb};
+  const uint32_t lo = (uint32_t)S.s0, hi = (uint32_t)(S.s0 >> 32);
   memcpy(&w[31 * stride], &iv[0], 4);
   memcpy(&w[32 * stride], &iv[1], 4);
   memcpy(&w[33 * stride], &lo, 4);
@@ -435,9 +435,27 @@ PGG_COLD bool record_valid_d(const float4& vy, const V3<float>& x, const V3<floa
   return distd > 1e-9 && dot(omd, cvt<double>(n)) > 1e-9;
 }
 
+// VPL accessors for the record loop: straight from global memory (L2), or
+// from a shared-memory tile (own 32 x 8 block + EM halo) staged by TMA.
+struct VplGlobal {
+  const float* y;
+  const float* L;
+  int width, row0;
+  PGG_MHD float4 get_y(int cx, int cy) const { return ld4(y, (int64_t)(cy - row0) * width + cx); }
+  PGG_MHD float4 get_L(int cx, int cy) const { return ld4(L, (int64_t)(cy - row0) * width + cx); }
+};
+struct VplTile {
+  const float4* y;  // shared memory, [rows][cols]
+  const float4* L;
+  int x0, y0, cols;  // frame coordinates of tile element (0, 0)
+  PGG_MHD float4 get_y(int cx, int cy) const { return y[(cy - y0) * cols + (cx - x0)]; }
+  PGG_MHD float4 get_L(int cx, int cy) const { return L[(cy - y0) * cols + (cx - x0)]; }
+};
+
 // One training record (guide_buffers.py:186-230): receiver S, VPL (y, L).
 // Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y.
-PGG_HD void em_record(const EmSetup& S, const float4& vy, const PassArgs& A, int64_t vi, float* acc) {
+template <class VS>
+PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
   const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
   const float dist2 = dot(d, d);
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
@@ -454,7 +472,7 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const PassArgs& A, int
     return;
   }
   const float cr = dl.z;
-  const float4 lv = ld4(A.vpl.L, vi);
+  const float4 lv = V.get_L(cx, cy);
   float w, bp;
   if (!(S.flags & 2)) {
     // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
@@ -499,7 +517,8 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const PassArgs& A, int
 // Slot 0 is the pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and
 // u2 = draw 18+s of the pixel's stream (the reference draws all 19 u1 then
 // all 19 u2, guide_buffers.py:144-145) and rounds the disk offset.
-PGG_HD void em_partial(const PassArgs& A, const EmSetup& S, int x, int y, int j, const uint64_t* jmul,
+template <class VS>
+PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, int j, const uint64_t* jmul,
                        const uint64_t* jadd, float* acc) {
   const pgg_config& C = A.cfg;
   const int W = C.width, H = C.height;
@@ -511,9 +530,8 @@ PGG_HD void em_partial(const PassArgs& A, const EmSetup& S, int x, int y, int j,
       if (y < vr0 || y >= vr1) {
         count_miss(A.halo_misses);
       } else {
-        const int64_t vi = (int64_t)(y - vr0) * W + x;
-        const float4 vy = ld4(A.vpl.y, vi);
-        if (vy.w != 0.0f) em_record(S, vy, A, vi, acc);
+        const float4 vy = V.get_y(x, y);
+        if (vy.w != 0.0f) em_record(S, vy, V, x, y, acc);
       }
     }
     s = EM_LANES;
@@ -533,10 +551,9 @@ PGG_HD void em_partial(const PassArgs& A, const EmSetup& S, int x, int y, int j,
       count_miss(A.halo_misses);
       continue;
     }
-    const int64_t vi = (int64_t)(cy - vr0) * W + cx;
-    const float4 vy = ld4(A.vpl.y, vi);
+    const float4 vy = V.get_y(cx, cy);
     if (vy.w == 0.0f) continue;  // VPL invalid or not BRDF-strategy
-    em_record(S, vy, A, vi, acc);
+    em_record(S, vy, V, cx, cy, acc);
   }
 }
 
@@ -672,9 +689,10 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl, const uint64_t* jmul, c
   float4 o0 = g0, o1 = g1;
   if (train) {
     float p[EM_LANES][7];
+    const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
     for (int j = 0; j < EM_LANES; ++j) {
       for (int k = 0; k < 7; ++k) p[j][k] = 0.0f;
-      em_partial(A, S, x, A.cfg.row0 + yl, j, jmul, jadd, p[j]);
+      em_partial(A, V, S, x, A.cfg.row0 + yl, j, jmul, jadd, p[j]);
     }
     float acc[7];
     em_combine(p, acc);
