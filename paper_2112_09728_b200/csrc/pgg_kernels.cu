@@ -222,10 +222,11 @@ bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int
 template <bool kTile>
 int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
   const SmemLayout SL(R, kTile);
-  static bool attr_set[MAX_TILE_R + 1] = {};
-  if (SL.total > 48 * 1024 && !attr_set[R]) {
-    cudaFuncSetAttribute(k_guiding_pass<kTile>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SL.total);
-    attr_set[R] = true;
+  static bool attr_set = false;  // opt in once to the largest layout this instantiation can use
+  if (!attr_set) {
+    const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);
+    cudaFuncSetAttribute(k_guiding_pass<kTile>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
+    attr_set = true;
   }
   const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
   k_guiding_pass<kTile><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);

@@ -375,14 +375,9 @@ PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
   const float mx = fmaxf(ax, ay);
   const float t = mx > 0.0f ? r_div(fminf(ax, ay), mx) : 0.0f;
   const float u = atan_unit(t) * (4.0f * 0.31830988618379067154f) * rho;
-  float a, b;
-  if (ax >= ay) {
-    a = copysignf(rho, x);
-    b = copysignf(u, y);
-  } else {
-    a = copysignf(u, x);
-    b = copysignf(rho, y);
-  }
+  const bool xdom = ax >= ay;
+  const float a = copysignf(xdom ? rho : u, x);
+  const float b = copysignf(xdom ? u : rho, y);
   sx = fminf(fmaxf((a + 1.0f) * 0.5f, 0.0f), 1.0f);
   sy = fminf(fmaxf((b + 1.0f) * 0.5f, 0.0f), 1.0f);
 }
