@@ -79,7 +79,8 @@ PGG_HD float r_rsqrt(float x) {
 }
 PGG_HD float r_div(float a, float b) {
 #ifdef __CUDA_ARCH__
-  const float r = __frcp_rn(b);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
   const float q = a * r;
   return fmaf(r, fmaf(-b, q, a), q);
 #else
