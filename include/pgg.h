@@ -11,6 +11,7 @@
  *                          ptrace._sample_first_bounce  ptrace.py:161-220 (+ the
  *                          per-pixel lane setup of ptrace.py:449-475)
  *                          any subset of the three, fused into one kernel
+ *   pgg_train_records .... guide_buffers.gather_training_batch  guide_buffers.py:234-259
  *   pgg_sample_lanes ..... ptrace._sample_first_bounce  ptrace.py:161-220 and
  *                          mixture.sample_mixture       mixture.py:193-259 on
  *                          caller-owned PCG32 states (in/out)
@@ -126,6 +127,14 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
                      const pgg_gamma_in* gamma_prev, const pgg_vpl* vpl, const pgg_gamma_out* gamma_reproj,
                      const pgg_gamma_out* gamma_out, const pgg_samples* samples, int32_t* halo_misses,
                      void* stream);
+
+/* Training records of n pixels (pix_xy: n x int32 (x, y)) for
+ * guide_buffers.gather_training_batch (guide_buffers.py:234-259): the EM
+ * candidate draws come from the caller's per-pixel PCG32 states (states is
+ * W*H, indexed by pixel, not advanced here).  records: n x 20 x float4
+ * (sq_x, sq_y, weight, valid) in slot order. */
+int pgg_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma, const pgg_vpl* vpl,
+                      int64_t n, const int32_t* pix_xy, const uint64_t* states, float* records, void* stream);
 
 /* Per-lane depth-0 sampling on caller-owned PCG32 states (in/out).
  * Inputs per lane: normal/view float4 (w unused), roughness, glossy (u8),

@@ -282,6 +282,18 @@ __global__ void k_sample_lanes(int64_t n, int world, const float4* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// training-record dump (gather_training_batch)
+
+__global__ void k_train_records(const PassArgs A, int64_t n, const int32_t* __restrict__ pix_xy,
+                                const uint64_t* __restrict__ states, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = pix_xy[2 * i], y = pix_xy[2 * i + 1];
+  const uint64_t s0 = states[(int64_t)y * A.cfg.width + x];
+  em_dump(A, x, y, s0, c_jmul, c_jadd, out + i * SLOTS * 4);
+}
+
+// ---------------------------------------------------------------------------
 // small batch kernels of the API edge
 
 __global__ void k_lobe(int64_t n, const double* __restrict__ st, double* mu, double* cov, double* chol, double* z,
@@ -493,6 +505,22 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
       encode_vpl_map(&ml, vpl->L, cfg->width, vpl->rows, R))
     return launch_pass<true>(A, my, ml, R, S(stream));
   return launch_pass<false>(A, my, ml, 0, S(stream));
+}
+
+int pgg_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma, const pgg_vpl* vpl,
+                      int64_t n, const int32_t* pix_xy, const uint64_t* states, float* records, void* stream) {
+  if (!cfg || !cur || !gamma || !vpl || n < 0 || !pix_xy || !states || !records || cfg->k_max < 1)
+    return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  PassArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cfg = *cfg;
+  A.cur = *cur;
+  A.gin = *gamma;
+  A.vpl = *vpl;
+  A.has_vpl = 1;
+  k_train_records<<<blocks(n, 64), 64, 0, S(stream)>>>(A, n, pix_xy, states, records);
+  return check_launch();
 }
 
 int pgg_sample_lanes(int64_t n, int32_t world, const float* normal, const float* view, const float* rough,

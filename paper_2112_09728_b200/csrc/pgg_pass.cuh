@@ -453,64 +453,80 @@ struct VplTile {
 };
 
 // One training record (guide_buffers.py:186-230): receiver S, VPL (y, L).
-// Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y.
-template <class VS>
-PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
+// Returns the reference's geometric validity (dist > 1e-9, cos > 1e-9) and
+// fills w (luminance weight), r (E-step responsibility) and the square
+// point; kAll also evaluates records whose weight is known to be zero
+// (view below the surface), which the accumulating path skips.
+struct Rec {
+  float w, r, qx, qy;
+};
+
+template <bool kAll, class VS>
+PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, Rec& o) {
   const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
   const float dist2 = dot(d, d);
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
   const V3<float> om = d * rinv;
   const V3<float> dl = S.fr.to_local(om);
   if (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f) {
-    if (!record_valid_d(vy, S.x, S.n_raw)) return;
+    if (!record_valid_d(vy, S.x, S.n_raw)) return false;
   } else if (!(dl.z > 1e-9f)) {
-    return;
+    return false;
   }
   const bool co_pos = (S.flags & 4) != 0;
-  if (!co_pos) {
-    // f = 0 and brdf_pdf = 0: a valid, zero-weight record
-    return;
-  }
+  o.w = 0.0f;
+  o.r = 0.0f;
+  if (!co_pos && !kAll) return true;  // f = 0 and brdf_pdf = 0: zero weight
   const float cr = dl.z;
-  const float4 lv = V.get_L(cx, cy);
-  float w, bp;
-  if (!(S.flags & 2)) {
-    // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
-    bp = cr * K<float>::inv_pi;
-    w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
-  } else {
-    // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
-    const V3<float> hr = dl + S.wol;
-    const float D = ggx_d_fast(S.a2, S.kappa, hr);
-    bp = S.g1o * D;
-    const float spec = bp * ggx_g1_fast(S.a2, cr);
-    const float hi = fabsf(dot(hr, dl)) * m_rsqrt(fmaxf(dot(hr, hr), 1e-30f));
-    const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
-    const float t2 = t * t;
-    const float f5 = t2 * t2 * t;
-    const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
-    const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
-    const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
-    // f cos = F D G1(wi) G1(wo) / (4 cos_i cos_o) * cos_i
-    w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+  float bp = 0.0f;
+  if (co_pos) {
+    const float4 lv = V.get_L(cx, cy);
+    if (!(S.flags & 2)) {
+      // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
+      bp = cr * K<float>::inv_pi;
+      o.w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
+    } else {
+      // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
+      const V3<float> hr = dl + S.wol;
+      const float D = ggx_d_fast(S.a2, S.kappa, hr);
+      bp = S.g1o * D;
+      const float spec = bp * ggx_g1_fast(S.a2, cr);
+      const float hi = fabsf(dot(hr, dl)) * m_rsqrt(fmaxf(dot(hr, hr), 1e-30f));
+      const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
+      const float t2 = t * t;
+      const float f5 = t2 * t2 * t;
+      const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
+      const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
+      const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
+      // f cos = F D G1(wi) G1(wo) / (4 cos_i cos_o) * cos_i
+      o.w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+    }
+    if (!kAll && !(isfinite(o.w) && o.w >= 0.0f)) return true;  // dropped by the M-step
   }
-  if (!(isfinite(w) && w >= 0.0f)) return;
-  float qx, qy;
-  dir_to_sq_f(dl, qx, qy);
-  const float z1 = (qx - S.mx) * S.il11;
-  const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+  dir_to_sq_f(dl, o.qx, o.qy);
+  const float z1 = (o.qx - S.mx) * S.il11;
+  const float z2 = ((o.qy - S.my) - S.l21 * z1) * S.il22;
   const float g = f_exp(-0.5f * (z1 * z1 + z2 * z2)) * S.gnorm;
   const float num = S.pi * g;
   const float den = num + (1.0f - S.pi) * bp;
-  const float r = den > 0.0f ? f_div(num, den) : 0.0f;
-  const float wr = w * r;
-  acc[0] += w;
+  o.r = den > 0.0f ? f_div(num, den) : 0.0f;
+  return true;
+}
+
+// Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y.
+template <class VS>
+PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
+  Rec o;
+  if (!em_eval<false>(S, vy, V, cx, cy, o)) return;
+  if (!(o.w > 0.0f) || !isfinite(o.w)) return;  // zero or dropped weights add nothing
+  const float wr = o.w * o.r;
+  acc[0] += o.w;
   acc[1] += wr;
-  acc[2] = fmaf(wr, qx, acc[2]);
-  acc[3] = fmaf(wr, qy, acc[3]);
-  acc[4] = fmaf(wr * qx, qx, acc[4]);
-  acc[5] = fmaf(wr * qy, qy, acc[5]);
-  acc[6] = fmaf(wr * qx, qy, acc[6]);
+  acc[2] = fmaf(wr, o.qx, acc[2]);
+  acc[3] = fmaf(wr, o.qy, acc[3]);
+  acc[4] = fmaf(wr * o.qx, o.qx, acc[4]);
+  acc[5] = fmaf(wr * o.qy, o.qy, acc[5]);
+  acc[6] = fmaf(wr * o.qx, o.qy, acc[6]);
 }
 
 // Partial sums of lane j of a pixel's 4-lane group: slots j, j+4, j+8, ... < N.
@@ -584,6 +600,32 @@ PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, i
   o1.w = (float)(k + 1.0);
 }
 
+// EM context of a valid pixel from its G-buffer planes, frame and lobe
+PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool glossy, const PixelFrame& pf,
+                     const LobeF& L, float k, int kmax, uint64_t s0, EmSetup& S) {
+  const double r2d = (double)pr.w * (double)pr.w;
+  const float alpha = (float)fmax(r2d, 1e-6);
+  S.x = v3(pr.x, pr.y, pr.z);
+  S.fr = pf.fr;
+  S.wol = pf.wol;
+  S.alb_r = va.w;
+  S.alb_g = am.x;
+  S.alb_b = am.y;
+  S.a2 = alpha * alpha;
+  S.kappa = kappa_world(pf.om_nn, S.a2);
+  S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
+  S.mx = L.mx;
+  S.my = L.my;
+  S.il11 = L.il11;
+  S.l21 = L.l21;
+  S.il22 = L.il22;
+  S.gnorm = L.gnorm;
+  S.pi = L.pi;
+  S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
+  S.nb = neighbor_budget(k, kmax);
+  S.s0 = s0;
+}
+
 // ---------------------------------------------------------------------------
 // Stage 1 of a pixel (own band, y_local yl): Gamma (reprojected or read),
 // optional reprojection output, depth-0 samples, and the EM context.
@@ -653,29 +695,57 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     }
   }
   if (!A.has_vpl) return false;
-  const double r2d = (double)rough * (double)rough;
-  const float alpha = (float)fmax(r2d, 1e-6);
-  S.x = v3(pr.x, pr.y, pr.z);
-  S.fr = pf.fr;
+  em_setup(pr, va, am, glossy, pf, L, g1.w, C.k_max, pcg_lane(C.key_train, pix), S);
   S.n_raw = n;
-  S.wol = pf.wol;
-  S.alb_r = va.w;
-  S.alb_g = am.x;
-  S.alb_b = am.y;
-  S.a2 = alpha * alpha;
-  S.kappa = kappa_world(pf.om_nn, S.a2);
-  S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
-  S.mx = L.mx;
-  S.my = L.my;
-  S.il11 = L.il11;
-  S.l21 = L.l21;
-  S.il22 = L.il22;
-  S.gnorm = L.gnorm;
-  S.pi = L.pi;
-  S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
-  S.nb = neighbor_budget(g1.w, C.k_max);
-  S.s0 = pcg_lane(C.key_train, pix);
   return true;
+}
+
+// Record dump of one pixel for gather_training_batch (guide_buffers.py:234-259):
+// Gamma from gamma_in, EM stream state `s0` supplied by the caller; writes
+// per slot (qx, qy, w, valid) for slots < N, valid = 0 beyond.
+PGG_HD void em_dump(const PassArgs& A, int x, int y, uint64_t s0, const uint64_t* jmul, const uint64_t* jadd,
+                    float* out) {
+  const pgg_config& C = A.cfg;
+  const int W = C.width, H = C.height;
+  for (int s = 0; s < SLOTS; ++s) {
+    out[4 * s + 0] = 0.5f;
+    out[4 * s + 1] = 0.5f;
+    out[4 * s + 2] = 0.0f;
+    out[4 * s + 3] = 0.0f;
+  }
+  const int64_t ci = (int64_t)(y - A.cur.row0) * W + x;
+  const uint8_t fl = ldu8(A.cur.flags, ci);
+  if (!(fl & 1)) return;
+  const float4 nd = ld4(A.cur.nd, ci), pr = ld4(A.cur.pr, ci), va = ld4(A.cur.va, ci), am = ld4(A.cur.am, ci);
+  const int64_t gi = (int64_t)(y - A.gin.row0) * W + x;
+  const float4 g0 = ld4(A.gin.g0, gi), g1 = ld4(A.gin.g1, gi);
+  const LobeF L = make_lobe(g0.x, g0.y, g0.z, g0.w, g1.x, g1.z);
+  const PixelFrame pf = make_pixel_frame(v3(nd.x, nd.y, nd.z), v3(va.x, va.y, va.z));
+  EmSetup S;
+  em_setup(pr, va, am, (fl & 4) != 0, pf, L, g1.w, C.k_max, s0, S);
+  S.n_raw = v3(nd.x, nd.y, nd.z);
+  const VplGlobal V{A.vpl.y, A.vpl.L, W, A.vpl.row0};
+  for (int s = 0; s < S.nb; ++s) {
+    int cx = x, cy = y;
+    if (s > 0) {
+      const uint32_t ua = pcg_out(jmul[s - 1] * s0 + jadd[s - 1]);
+      const uint32_t ub = pcg_out(jmul[s + 18] * s0 + jadd[s + 18]);
+      int dx, dy;
+      disk_offset(ua, ub, C.radius, dx, dy);
+      cx += dx;
+      cy += dy;
+      if (cx < 0 || cx >= W || cy < 0 || cy >= H) continue;
+    }
+    if (cy < A.vpl.row0 || cy >= A.vpl.row0 + A.vpl.rows) continue;
+    const float4 vy = V.get_y(cx, cy);
+    if (vy.w == 0.0f) continue;
+    Rec o;
+    if (!em_eval<true>(S, vy, V, cx, cy, o)) continue;
+    out[4 * s + 0] = o.qx;
+    out[4 * s + 1] = o.qy;
+    out[4 * s + 2] = o.w;
+    out[4 * s + 3] = 1.0f;
+  }
 }
 
 // Whole pixel on one thread (host build): the device splits stage 2 over a
