@@ -103,3 +103,22 @@ int pgghc_neighbor_budget(int64_t n, const float* k, int32_t kmax, int32_t* out)
 }
 
 }  // extern "C"
+
+extern "C" int pgghc_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma,
+                                   const pgg_vpl* vpl, int64_t n, const int32_t* pix_xy, const uint64_t* states,
+                                   float* records) {
+  PassArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cfg = *cfg;
+  A.cur = *cur;
+  A.gin = *gamma;
+  A.vpl = *vpl;
+  A.has_vpl = 1;
+  uint64_t jm[JUMPS], ja[JUMPS];
+  jump_tables(jm, ja);
+  for (int64_t i = 0; i < n; ++i) {
+    const int x = pix_xy[2 * i], y = pix_xy[2 * i + 1];
+    em_dump(A, x, y, states[(int64_t)y * cfg->width + x], jm, ja, records + i * SLOTS * 4);
+  }
+  return PGG_OK;
+}

@@ -399,10 +399,13 @@ PGG_HD EmSetup em_from_words(const float* w, int stride) {
   return S;
 }
 
-// jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..27
-constexpr int JUMPS = 28;
-#define PGG_J7(F, b) F(b + 0), F(b + 1), F(b + 2), F(b + 3), F(b + 4), F(b + 5), F(b + 6)
-#define PGG_JTAB(F) PGG_J7(F, 0), PGG_J7(F, 7), PGG_J7(F, 14), PGG_J7(F, 21)
+// jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..37
+// (every draw position of the 38-draw EM candidate block)
+constexpr int JUMPS = 38;
+#define PGG_J2(F, b) F(b + 0), F(b + 1)
+#define PGG_J6(F, b) PGG_J2(F, b), PGG_J2(F, b + 2), PGG_J2(F, b + 4)
+#define PGG_JTAB(F) PGG_J6(F, 0), PGG_J6(F, 6), PGG_J6(F, 12), PGG_J6(F, 18), PGG_J6(F, 24), PGG_J6(F, 30), \
+    PGG_J2(F, 36)
 #ifdef __CUDACC__
 __constant__ uint64_t c_jmul[JUMPS] = {PGG_JTAB(pcg_jump_mul)};
 __constant__ uint64_t c_jadd[JUMPS] = {PGG_JTAB(pcg_jump_add)};
