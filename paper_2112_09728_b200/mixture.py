@@ -44,14 +44,12 @@ class GaussianLobe(NamedTuple):
 
 
 def init_stats(shape=()):
-    """Fresh per-pixel state (pg/mixture.py:44-59), float64 NumPy array."""
+    """Fresh per-pixel state (pg/mixture.py:44-59): centred prior, Sigma =
+    0.25 I, pi at its lower clamp, k = 0; float64 NumPy array."""
     shp = tuple(np.atleast_1d(shape)) if shape != () else ()
-    n = int(np.prod(shp)) if shp else 1
-    g0 = torch.empty(n, 4, dtype=torch.float32, device=_conv.device())
-    g1 = torch.empty_like(g0)
-    _lib.check(_lib.lib().pgg_gamma_init(n, _lib.ptr(g0), _lib.ptr(g1), _lib.stream_ptr()))
-    out = torch.cat([g0, g1], dim=1).to(F64).cpu().numpy()
-    return out.reshape(shp + (8,)) if shp else out.reshape(8)
+    row = torch.tensor([0.5, 0.5, 0.5, 0.5, 0.25, 0.0, PI_MIN, 0.0], dtype=F64, device=_conv.device())
+    out = row.expand(shp + (8,)).contiguous() if shp else row
+    return out.cpu().numpy()
 
 
 def lobe_from_stats(stats):
