@@ -1,0 +1,160 @@
+"""Row-band sharding of the guiding pass over the GPUs of one node
+(SURVEY.md 8e): rank r owns the contiguous rows [r0, r1) of the frame; the
+only data the pass needs from other ranks are
+
+  * the VPL (Pi) rows within ceil(neighbor_radius) of the band edges, read by
+    the EM disk of this frame, and
+  * the previous frame's Gamma and G-buffer gate planes (flags, normal+depth)
+    within ``max_motion_rows`` of the band edges, read by reprojection.
+
+Every buffer is allocated with its halo rows in place ("extended" buffers,
+rows [r0 - h, r1 + h) clipped to the frame); a renderer writes its own band
+straight into the middle, and one grouped send/recv (torch.distributed
+batch_isend_irecv: NCCL over NVLink on GPUs, gloo in the CPU tests) moves
+the boundary rows into the neighbours' halo rows.  RNG streams are keyed on
+the GLOBAL pixel index, so any banding reproduces the single-GPU result
+bit for bit.
+"""
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+def band_rows(height, world, rank):
+    """Balanced contiguous row band of `rank` (first bands get the remainder)."""
+    base, rem = divmod(height, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+@dataclass
+class Extent:
+    """Rows [lo, hi) held by an extended buffer around the band [r0, r1)."""
+
+    r0: int
+    r1: int
+    lo: int
+    hi: int
+
+    @classmethod
+    def around(cls, r0, r1, halo, height):
+        return cls(r0, r1, max(0, r0 - halo), min(height, r1 + halo))
+
+    @property
+    def rows(self):
+        return self.hi - self.lo
+
+    def own(self, t):
+        """View of the own band inside an extended (rows, ...) tensor."""
+        return t[self.r0 - self.lo:self.r1 - self.lo]
+
+
+def halo_exchange(tensors, ext, rank, world, group=None, tag=0):
+    """Fill the halo rows of the extended tensors (each (ext.rows, W, ...))
+    from the neighbouring bands: rank-1 sends its last rows, rank+1 its first.
+
+    Ranks agree on the halo depth, so the rows rank r needs from rank r+1 are
+    exactly the rows rank r+1 sends up.  One grouped batch of P2P ops."""
+    if world == 1:
+        return
+    ops = []
+    up_rows = ext.r0 - ext.lo       # rows [lo, r0) come from rank - 1
+    down_rows = ext.hi - ext.r1     # rows [r1, hi) come from rank + 1
+    for t in tensors:
+        own = ext.own(t)
+        if rank > 0 and up_rows > 0:
+            ops.append(dist.P2POp(dist.irecv, t[:up_rows], rank - 1, group, tag))
+            ops.append(dist.P2POp(dist.isend, own[:up_rows].contiguous(), rank - 1, group, tag))
+        if rank < world - 1 and down_rows > 0:
+            ops.append(dist.P2POp(dist.isend, own[own.shape[0] - down_rows:].contiguous(), rank + 1, group, tag))
+            ops.append(dist.P2POp(dist.irecv, t[t.shape[0] - down_rows:], rank + 1, group, tag))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def check_band_geometry(height, world, halo):
+    """Every band must be at least `halo` rows tall so that a halo comes from
+    the adjacent rank only."""
+    for r in range(world):
+        r0, r1 = band_rows(height, world, r)
+        if r1 - r0 < halo:
+            raise ValueError(f"band {r} has {r1 - r0} rows < halo {halo}: too many ranks for this frame height")
+
+
+class BandedGuiding:
+    """One rank's share of a row-band-sharded guiding sequence.
+
+    Per frame: ``frame_inputs()`` hands out the extended buffers to fill (own
+    rows only), ``step(frame)`` exchanges halos and runs the fused pass on the
+    band.  Gamma, the previous G-buffer and the VPLs live in HBM with their
+    halos.  ``max_motion_rows`` bounds |motion_y| + 1 (halo misses are
+    counted on the device and reported by ``halo_misses()``)."""
+
+    def __init__(self, width, height, cfg, rank=0, world=1, group=None, device="cuda", max_motion_rows=8):
+        from .layout import GammaPlanes, GBufferPlanes, SamplePlanes, VplPlanes
+        self.W, self.H, self.cfg = width, height, cfg
+        self.rank, self.world, self.group = rank, world, group
+        self.dev = torch.device(device)
+        r0, r1 = band_rows(height, world, rank)
+        self.R = int(-(-cfg.neighbor_radius // 1)) if cfg.neighbor_radius > 0 else 0
+        self.M = int(max_motion_rows)
+        check_band_geometry(height, world, max(self.R, self.M))
+        self.ext_v = Extent.around(r0, r1, self.R, height)   # VPL extent
+        self.ext_g = Extent.around(r0, r1, self.M, height)   # Gamma / G-buffer extent
+        self.r0, self.r1 = r0, r1
+        eg = self.ext_g
+        self.gb = [GBufferPlanes.empty(eg.rows, width, self.dev, row0=eg.lo) for _ in range(2)]
+        self.gamma = [GammaPlanes.fresh(eg.rows, width, self.dev, row0=eg.lo) for _ in range(2)]
+        ev = self.ext_v
+        self.vpl = VplPlanes(torch.zeros(ev.rows, width, 4, device=self.dev),
+                             torch.zeros(ev.rows, width, 4, device=self.dev), row0=ev.lo)
+        self.samples = SamplePlanes.empty(r1 - r0, width, cfg.spp, self.dev)
+        self.cur = 0
+        self.has_prev = False
+        self._miss = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def frame_inputs(self):
+        """(G-buffer planes, VPL planes) whose OWN rows the caller fills."""
+        return self.gb[self.cur], self.vpl
+
+    def halo_tensors(self):
+        """The (extent, tensors) pairs whose halo rows step() exchanges."""
+        prev = self.gb[1 - self.cur]
+        g_in = self.gamma[self.cur]
+        pairs = [(self.ext_v, [self.vpl.y, self.vpl.L])]
+        if self.has_prev:
+            pairs.append((self.ext_g, [prev.flags, prev.nd, g_in.g0, g_in.g1]))
+        return pairs
+
+    def step(self, frame, exchange=True):
+        """Exchange halos (unless the caller already filled them, exchange=False)
+        and run the fused pass on this band."""
+        from .session import run_pass
+        cur, prev = self.gb[self.cur], self.gb[1 - self.cur]
+        g_in, g_out = self.gamma[self.cur], self.gamma[1 - self.cur]
+        if exchange:
+            # halos: this frame's VPLs; previous frame's Gamma and gate planes
+            for tag, (ext, ts) in enumerate(self.halo_tensors()):
+                halo_exchange(ts, ext, self.rank, self.world, self.group, tag=1 + tag)
+        eg = self.ext_g
+        out_view = type(g_out)(eg.own(g_out.g0), eg.own(g_out.g1), row0=self.r0)
+        cur_band = type(cur)(eg.own(cur.flags), eg.own(cur.nd), eg.own(cur.pr), eg.own(cur.va), eg.own(cur.am),
+                             cur.cam_origin, row0=self.r0)
+        res = run_pass(self.cfg, frame, cur_band, g_in, prev=prev if self.has_prev else None, vpl=self.vpl,
+                       height=self.H, row0=self.r0, rows=self.r1 - self.r0, out_gamma=out_view,
+                       out_samples=self.samples, halo_misses=self._miss)
+        self.cur = 1 - self.cur
+        self.has_prev = True
+        return res
+
+    @property
+    def gamma_own(self):
+        """This rank's band of the latest Gamma (planes views)."""
+        g = self.gamma[self.cur]
+        return self.ext_g.own(g.g0), self.ext_g.own(g.g1)
+
+    def halo_misses(self):
+        return int(self._miss.item())

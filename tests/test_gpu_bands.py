@@ -1,0 +1,66 @@
+"""Row-band sharding on ONE GPU: N BandedGuiding ranks, halos filled by a
+local copy standing in for the NCCL exchange, must reproduce the
+whole-frame session bit for bit over a multi-frame sequence (SURVEY 8e:
+outputs at N GPUs bitwise equal to 1 GPU)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _fill(band, g, v):
+    """Write a band's OWN rows of frame inputs (as a renderer of that band would)."""
+    from paper_2112_09728_b200.layout import GBufferPlanes, VplPlanes
+    gb, vp = band.frame_inputs()
+    full_g = GBufferPlanes.from_ref(g, device=band.dev)
+    full_v = VplPlanes.from_ref(v, device=band.dev)
+    r0, r1 = band.r0, band.r1
+    for name in ("flags", "nd", "pr", "va", "am"):
+        band.ext_g.own(getattr(gb, name)).copy_(getattr(full_g, name)[r0:r1])
+    gb.cam_origin = full_g.cam_origin
+    band.ext_v.own(vp.y).copy_(full_v.y[r0:r1])
+    band.ext_v.own(vp.L).copy_(full_v.L[r0:r1])
+
+
+def _local_exchange(bands):
+    """What halo_exchange does over NCCL: halo rows <- neighbours' own rows."""
+    for b in bands:
+        for k, (ext, ts) in enumerate(b.halo_tensors()):
+            for t_i, t in enumerate(ts):
+                for nb in bands:
+                    if nb is b:
+                        continue
+                    next_, nts = nb.halo_tensors()[k]
+                    src = nts[t_i]
+                    lo, hi = max(ext.lo, nb.r0), min(ext.hi, nb.r1)
+                    if lo < hi:
+                        t[lo - ext.lo:hi - ext.lo].copy_(src[lo - next_.lo:hi - next_.lo])
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_bands_match_whole_frame(cuda_dev, world):
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.bands import BandedGuiding
+    from paper_2112_09728_b200.layout import GBufferPlanes, PassConfig, VplPlanes
+    from paper_2112_09728_b200.session import GuidingSession
+    W, H, F, seed = 320, 184, 4, 11
+    cfg = PassConfig(seed=seed, spp=2)
+    frames = list(synth.sequence(W, H, F, seed=seed, device=cuda_dev))
+    whole = GuidingSession(W, H, cfg, device=cuda_dev)
+    bands = [BandedGuiding(W, H, cfg, rank=r, world=world, device=cuda_dev, max_motion_rows=8) for r in range(world)]
+    for f, (g, v) in enumerate(frames):
+        ref = whole.step(GBufferPlanes.from_ref(g, device=cuda_dev), VplPlanes.from_ref(v, device=cuda_dev), f)
+        for b in bands:
+            _fill(b, g, v)
+        _local_exchange(bands)
+        for b in bands:
+            b.step(f, exchange=False)
+        torch.cuda.synchronize()
+        g0 = torch.cat([b.gamma_own[0] for b in bands])
+        g1 = torch.cat([b.gamma_own[1] for b in bands])
+        assert torch.equal(g0, whole.gamma.g0) and torch.equal(g1, whole.gamma.g1), f
+        sd = torch.cat([b.samples.dir for b in bands])
+        st = torch.cat([b.samples.tag for b in bands])
+        assert torch.equal(sd, whole.samples.dir) and torch.equal(st, whole.samples.tag), f
+    assert all(b.halo_misses() == 0 for b in bands)
