@@ -38,7 +38,7 @@ BYTES_PER_EXTRA_SPP = 17
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=32)
+    ap.add_argument("--steps", type=int, default=160)
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--spp", type=int, default=1)
@@ -65,14 +65,15 @@ class ClockSampler:
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []      # (host time, fields)
         self.proc = None
+        self.window = None  # (t0, t1) of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -81,7 +82,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -92,11 +96,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        rows = [r for _, r in self.rows]
+        if self.window:
+            # samples inside the timed region (+ one 20 ms sampling period either side)
+            t0, t1 = self.window
+            inside = [r for t, r in self.rows if t0 - 0.025 <= t <= t1 + 0.025]
+            rows = inside or rows[-3:]
+        sm = [float(r[0]) for r in rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 3 + i and r[3 + i].lower() == "active":
                     reasons.add(n)
@@ -206,15 +216,17 @@ def bench_ours(args, rank, world, local_rank):
         state["g"], state["s"] = r.gamma, state["g"]
         state["i"] = i + 1
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
+        time.sleep(0.1)
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        h0 = time.monotonic()
         t0.record(stream)
         for k in range(args.steps):
             ev[k][0].record(stream)
@@ -222,6 +234,8 @@ def bench_ours(args, rank, world, local_rank):
             ev[k][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize(dev)
+        clk.mark(h0, time.monotonic())
+        time.sleep(0.05)
     total_ms = t0.elapsed_time(t1)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
     if world > 1:
