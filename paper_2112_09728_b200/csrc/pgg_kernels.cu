@@ -55,8 +55,10 @@ struct SmemLayout {
     tile_bytes = tile ? (size_t)cols * rows * 16 : 0;
     off_l = (tile_bytes + 127) & ~(size_t)127;
     off_em = off_l + ((tile_bytes + 127) & ~(size_t)127);
-    off_sum = off_em + (size_t)TILE_H * EM_WORDS * TILE_W * 4;
-    off_bar = off_sum + (size_t)TILE_H * 7 * TILE_W * 4;
+    const size_t em_bytes = EM_LANES > 1 ? (size_t)TILE_H * EM_WORDS * TILE_W * 4 : 0;
+    const size_t sum_bytes = EM_LANES > 1 ? (size_t)TILE_H * 7 * TILE_W * 4 : 0;
+    off_sum = off_em + em_bytes;
+    off_bar = off_sum + sum_bytes;
     total = off_bar + 16;
   }
 };
@@ -139,6 +141,28 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
     S.flags = 0;
     S.nb = 0;
   }
+  if constexpr (EM_LANES == 1) {
+    // one lane per pixel end to end: the EM context stays in registers
+    if (kTile) mbar_wait(bar, 0);
+    if (!active) return;
+    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int y = A.cfg.row0 + yl;
+    if (train) {
+      if (kTile) {
+        const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
+        em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
+      } else {
+        const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
+        em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
+      }
+    }
+    const int64_t own = (int64_t)yl * A.cfg.width + x;
+    float4 o0 = g0, o1 = g1;
+    if (train) m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
+    st4(A.gout.g0, own, o0);
+    st4(A.gout.g1, own, o1);
+    return;
+  }
   float* my_em = s_em + warp * EM_WORDS * TILE_W;
   em_to_words(S, my_em + lane, TILE_W);
   __syncwarp();
@@ -164,8 +188,8 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
       float v = acc[k];
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
+#pragma unroll
+      for (int m = EM_LANES / 2; m >= 1; m /= 2) v += __shfl_xor_sync(0xffffffffu, v, m);
       acc[k] = v;
     }
     if (j == 0) {

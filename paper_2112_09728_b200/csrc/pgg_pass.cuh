@@ -419,7 +419,10 @@ PGG_HD void jump_tables(uint64_t* mul, uint64_t* add) {
     a = a * PCG_MUL + PCG_INC;
   }
 }
-constexpr int EM_LANES = 4;  // lanes per pixel in stage 2
+#ifndef PGG_EM_LANES
+#define PGG_EM_LANES 1  // measured on B200: 1 lane/pixel 0.757 ms, 2: 0.796, 4: 0.868, 8: 1.03 (1080p)
+#endif
+constexpr int EM_LANES = PGG_EM_LANES;  // lanes per pixel in stage 2
 constexpr uint64_t JL_MUL = pcg_jump_mul(EM_LANES);
 constexpr uint64_t JL_ADD = pcg_jump_add(EM_LANES);
 
@@ -576,10 +579,17 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   }
 }
 
-// The 4-lane butterfly order of the device reduction (xor 2, then 1), so
+// The butterfly order of the device reduction (xor EM_LANES/2, ..., 1), so
 // the host build sums in exactly the same order.
 PGG_HD void em_combine(float p[EM_LANES][7], float* out) {
-  for (int k = 0; k < 7; ++k) out[k] = (p[0][k] + p[2][k]) + (p[1][k] + p[3][k]);
+  for (int k = 0; k < 7; ++k) {
+    float v[EM_LANES];
+    for (int j = 0; j < EM_LANES; ++j) v[j] = p[j][k];
+    for (int m = EM_LANES / 2; m >= 1; m /= 2)
+      for (int j = 0; j < EM_LANES; ++j)
+        if (!(j & m)) v[j] = v[j] + v[j | m];  // lane j and j^m hold the same sum afterwards
+    out[k] = v[0];
+  }
 }
 
 // Online M-step (mixture.py:276-321) in float64 from the float32 sums.
