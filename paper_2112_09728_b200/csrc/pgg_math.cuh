@@ -52,6 +52,24 @@ PGG_HD float f_exp(float x) {
   return expf(x);
 #endif
 }
+PGG_HD float f_exp2(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return exp2f(x);
+#endif
+}
+PGG_HD float f_rcp(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return 1.0f / x;
+#endif
+}
 PGG_HD float f_div(float a, float b) {
 #ifdef __CUDA_ARCH__
   return __fdividef(a, b);

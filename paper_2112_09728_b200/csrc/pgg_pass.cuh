@@ -346,7 +346,7 @@ struct EmSetup {
   V3<float> wol;     // view in the local frame
   float alb_r, alb_g, alb_b;
   float a2, kappa, g1o;  // g1o = G1(cos_o) / (4 cos_o)
-  float mx, my, il11, l21, il22, gnorm, pi;
+  float mx, my, il11, l21, il22, gnorm, pi;  // il11, il22 x c and l21 / c, c = sqrt(log2(e) / 2)
   int flags;         // bit0 train this pixel, bit1 glossy, bit2 cos_o > 0
   int nb;            // neighbour budget N (mixture.py:324-328)
   uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
@@ -449,6 +449,10 @@ struct VplGlobal {
   int width, row0;
   PGG_MHD float4 get_y(int cx, int cy) const { return ld4(y, (int64_t)(cy - row0) * width + cx); }
   PGG_MHD float4 get_L(int cx, int cy) const { return ld4(L, (int64_t)(cy - row0) * width + cx); }
+  PGG_MHD int64_t index(int cx, int cy) const { return (int64_t)(cy - row0) * width + cx; }
+  PGG_MHD int stride() const { return width; }
+  PGG_MHD float4 y_at(int64_t i) const { return ld4(y, i); }
+  PGG_MHD float4 L_at(int64_t i) const { return ld4(L, i); }
 };
 struct VplTile {
   const float4* y;  // shared memory, [rows][cols]
@@ -456,6 +460,10 @@ struct VplTile {
   int x0, y0, cols;  // frame coordinates of tile element (0, 0)
   PGG_MHD float4 get_y(int cx, int cy) const { return y[(cy - y0) * cols + (cx - x0)]; }
   PGG_MHD float4 get_L(int cx, int cy) const { return L[(cy - y0) * cols + (cx - x0)]; }
+  PGG_MHD int index(int cx, int cy) const { return (cy - y0) * cols + (cx - x0); }
+  PGG_MHD int stride() const { return cols; }
+  PGG_MHD float4 y_at(int i) const { return y[i]; }
+  PGG_MHD float4 L_at(int i) const { return L[i]; }
 };
 
 // One training record (guide_buffers.py:186-230): receiver S, VPL (y, L).
@@ -512,30 +520,77 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
   dir_to_sq_f(dl, o.qx, o.qy);
   const float z1 = (o.qx - S.mx) * S.il11;
   const float z2 = ((o.qy - S.my) - S.l21 * z1) * S.il22;
-  const float g = f_exp(-0.5f * (z1 * z1 + z2 * z2)) * S.gnorm;
+  const float g = f_exp2(-(z1 * z1 + z2 * z2)) * S.gnorm;
   const float num = S.pi * g;
   const float den = num + (1.0f - S.pi) * bp;
-  o.r = den > 0.0f ? f_div(num, den) : 0.0f;
+  o.r = num * f_rcp(fmaxf(den, 1e-30f));  // den = 0 only with num = 0 -> r = 0
   return true;
 }
 
-// Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y.
-template <class VS>
-PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
-  Rec o;
-  if (!em_eval<false>(S, vy, V, cx, cy, o)) return;
-  if (!(o.w > 0.0f) || !isfinite(o.w)) return;  // zero or dropped weights add nothing
-  const float wr = o.w * o.r;
-  acc[0] += o.w;
+// Accumulates w, w r, w r x, w r y, w r x^2, w r y^2, w r x y of one record,
+// branch-light: the candidate's validity `ok` masks the sums instead of
+// branching (a warp with mixed validity pays the full record either way),
+// so the record and the next slot's draws form one schedulable block.
+template <class VS, class IDX>
+PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX idx, bool ok, float* acc) {
+  const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
+  const float dist2 = dot(d, d);
+  const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
+  const V3<float> dl = S.fr.to_local(d * rinv);
+  if (ok && (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f)) {
+    ok = record_valid_d(vy, S.x, S.n_raw);
+  } else {
+    ok = ok && dl.z > 1e-9f;
+  }
+  const float cr = fmaxf(dl.z, 0.0f);
+  const float4 lv = V.L_at(idx);
+  // Lambert (scene.py:269, 296)
+  float bp = cr * K<float>::inv_pi;
+  float w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
+  if (S.flags & 2) {
+    // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
+    const V3<float> hr = dl + S.wol;
+    const float D = ggx_d_fast(S.a2, S.kappa, hr);
+    bp = S.g1o * D;
+    const float spec = bp * ggx_g1_fast(S.a2, cr);
+    const float hi = fabsf(dot(hr, dl)) * m_rsqrt(fmaxf(dot(hr, hr), 1e-30f));
+    const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
+    const float t2 = t * t;
+    const float f5 = t2 * t2 * t;
+    const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
+    const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
+    const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
+    w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+  }
+  // non-finite or zero weights are dropped / add nothing (mixture.py:291)
+  ok = ok && w > 0.0f && w <= 3.402823466e38f;
+  float qx, qy;
+  dir_to_sq_f(dl, qx, qy);
+  const float z1 = (qx - S.mx) * S.il11;
+  const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+  const float g = f_exp2(-(z1 * z1 + z2 * z2)) * S.gnorm;
+  const float num = S.pi * g;
+  const float den = num + (1.0f - S.pi) * bp;
+  const float r = num * f_rcp(fmaxf(den, 1e-30f));
+  const float wv = ok ? w : 0.0f;
+  const float wr = ok ? w * r : 0.0f;
+  qx = ok ? qx : 0.0f;  // masked records may carry NaN from unused inputs
+  qy = ok ? qy : 0.0f;
+  acc[0] += wv;
   acc[1] += wr;
-  acc[2] = fmaf(wr, o.qx, acc[2]);
-  acc[3] = fmaf(wr, o.qy, acc[3]);
-  acc[4] = fmaf(wr * o.qx, o.qx, acc[4]);
-  acc[5] = fmaf(wr * o.qy, o.qy, acc[5]);
-  acc[6] = fmaf(wr * o.qx, o.qy, acc[6]);
+  acc[2] = fmaf(wr, qx, acc[2]);
+  acc[3] = fmaf(wr, qy, acc[3]);
+  acc[4] = fmaf(wr * qx, qx, acc[4]);
+  acc[5] = fmaf(wr * qy, qy, acc[5]);
+  acc[6] = fmaf(wr * qx, qy, acc[6]);
 }
 
-// Partial sums of lane j of a pixel's 4-lane group: slots j, j+4, j+8, ... < N.
+template <class VS>
+PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
+  em_accumulate(S, vy, V, V.index(cx, cy), true, acc);
+}
+
+// Partial sums of lane j of a pixel's group: slots j, j + EM_LANES, ... < N.
 // Slot 0 is the pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and
 // u2 = draw 18+s of the pixel's stream (the reference draws all 19 u1 then
 // all 19 u2, guide_buffers.py:144-145) and rounds the disk offset.
@@ -543,19 +598,21 @@ template <class VS>
 PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, int j, const uint64_t* jmul,
                        const uint64_t* jadd, float* acc) {
   const pgg_config& C = A.cfg;
-  const int W = C.width, H = C.height;
-  const int vr0 = A.vpl.row0, vr1 = A.vpl.row0 + A.vpl.rows;
+  const unsigned W = (unsigned)C.width, H = (unsigned)C.height;
+  const int vr0 = A.vpl.row0;
+  const unsigned vrows = (unsigned)A.vpl.rows;
+  if (S.nb <= 0) return;
+  if ((unsigned)(y - vr0) >= vrows) {  // own row outside the VPL rows: every slot misses
+    count_miss(A.halo_misses);
+    return;
+  }
+  const auto base = V.index(x, y);
+  const int stride = V.stride();
   int s = j;
   uint64_t sa = 0, sb = 0;
   if (s == 0) {
-    if (S.nb > 0) {
-      if (y < vr0 || y >= vr1) {
-        count_miss(A.halo_misses);
-      } else {
-        const float4 vy = V.get_y(x, y);
-        if (vy.w != 0.0f) em_record(S, vy, V, x, y, acc);
-      }
-    }
+    const float4 vy = V.y_at(base);
+    em_accumulate(S, vy, V, base, vy.w != 0.0f, acc);
     s = EM_LANES;
   }
   if (s >= S.nb) return;
@@ -568,14 +625,15 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     int dx, dy;
     disk_offset(ua, ub, C.radius, dx, dy);
     const int cx = x + dx, cy = y + dy;
-    if (cx < 0 || cx >= W || cy < 0 || cy >= H) continue;
-    if (cy < vr0 || cy >= vr1) {
+    bool ok = (unsigned)cx < W && (unsigned)cy < H;
+    if (ok && (unsigned)(cy - vr0) >= vrows) {
       count_miss(A.halo_misses);
-      continue;
+      ok = false;
     }
-    const float4 vy = V.get_y(cx, cy);
-    if (vy.w == 0.0f) continue;  // VPL invalid or not BRDF-strategy
-    em_record(S, vy, V, cx, cy, acc);
+    const auto idx = ok ? base + (decltype(base))dy * stride + dx : base;
+    const float4 vy = V.y_at(idx);
+    ok = ok && vy.w != 0.0f;  // VPL invalid or not BRDF-strategy
+    em_accumulate(S, vy, V, idx, ok, acc);
   }
 }
 
@@ -613,6 +671,8 @@ PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, i
   o1.w = (float)(k + 1.0);
 }
 
+constexpr double GAUSS_C = 0.84932180028801904272;  // sqrt(log2(e) / 2)
+
 // EM context of a valid pixel from its G-buffer planes, frame and lobe
 PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool glossy, const PixelFrame& pf,
                      const LobeF& L, float k, int kmax, uint64_t s0, EmSetup& S) {
@@ -629,9 +689,10 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
   S.mx = L.mx;
   S.my = L.my;
-  S.il11 = L.il11;
-  S.l21 = L.l21;
-  S.il22 = L.il22;
+  // exponent -(z1^2 + z2^2)/2 evaluated as exp2(-(z1'^2 + z2'^2)) with z' = c z
+  S.il11 = (float)((double)L.il11 * GAUSS_C);
+  S.l21 = (float)((double)L.l21 / GAUSS_C);
+  S.il22 = (float)((double)L.il22 * GAUSS_C);
   S.gnorm = L.gnorm;
   S.pi = L.pi;
   S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
@@ -710,7 +771,9 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   if (!A.has_vpl) return false;
   em_setup(pr, va, am, glossy, pf, L, g1.w, C.k_max, pcg_lane(C.key_train, pix), S);
   S.n_raw = n;
-  return true;
+  // view below the surface: every record has f = 0, so the batch carries no
+  // weight and the reference leaves Gamma (and k) unchanged -- skip the EM
+  return pf.co_pos;
 }
 
 // Record dump of one pixel for gather_training_batch (guide_buffers.py:234-259):
