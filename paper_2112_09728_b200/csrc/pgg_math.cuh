@@ -604,10 +604,32 @@ struct LobeF {
   X(0.98736427798565474f, 0.01426569431446678f)      \
   X(0.99759360999851066f, 0.0061706148999943452f)
 
+// Fast standard normal CDF for the truncation mass: Phi(x) = erfc(-x/sqrt2)/2
+// with the Chebyshev-fitted erfc of Numerical Recipes (erfcc, fractional
+// error < 1.2e-7), ~15 instructions instead of normcdff's ~120.  Measured in
+// float32: <= 2.1e-7 absolute, <= 2e-6 relative for x >= -6.
+PGG_HD float ndtr_fast(float x) {
+  const float z = -x * 0.70710678118654752440f;
+  const float az = fabsf(z);
+  const float t = f_rcp(fmaf(0.5f, az, 1.0f));
+  float p = 0.17087277f;
+  p = fmaf(p, t, -0.82215223f);
+  p = fmaf(p, t, 1.48851587f);
+  p = fmaf(p, t, -1.13520398f);
+  p = fmaf(p, t, 0.27886807f);
+  p = fmaf(p, t, -0.18628806f);
+  p = fmaf(p, t, 0.09678418f);
+  p = fmaf(p, t, 0.37409196f);
+  p = fmaf(p, t, 1.00002368f);
+  p = fmaf(p, t, -1.26551223f);
+  const float e = t * f_exp(fmaf(-az, az, p));  // erfc(|z|)
+  return 0.5f * (z >= 0.0f ? e : 2.0f - e);
+}
+
 // Phi(hi) - Phi(lo), hi > lo, evaluated on the side that avoids cancellation
 PGG_HD float ndtr_diff(float hi, float lo) {
-  if (lo >= 0.0f) return m_ndtr(-lo) - m_ndtr(-hi);
-  return m_ndtr(hi) - m_ndtr(lo);
+  if (lo >= 0.0f) return ndtr_fast(-lo) - ndtr_fast(-hi);
+  return ndtr_fast(hi) - ndtr_fast(lo);
 }
 
 // Inner-CDF saturation state of one edge term on a segment: 0 = Phi ~ 0,

@@ -148,20 +148,22 @@ PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const floa
     return;
   }
   const int64_t sp = (int64_t)(sy - A.prev.row0) * C.width + sx;
-  if (!(ldu8(A.prev.flags, sp) & 1)) return;
+  const int64_t gi = (int64_t)(sy - A.gin.row0) * C.width + sx;
+  // the source's gate planes and Gamma in flight together
+  const uint8_t pfl = ldu8(A.prev.flags, sp);
+  const float4 ndp = ld4(A.prev.nd, sp);
+  float4 p0 = ld4(A.gin.g0, gi);
+  const float4 p1 = ld4(A.gin.g1, gi);
+  if (!(pfl & 1)) return;
   // depth and normal gates in float64, reference operation order
   const double dx = rsub((double)pr.x, C.prev_cam[0]);
   const double dy = rsub((double)pr.y, C.prev_cam[1]);
   const double dz = rsub((double)pr.z, C.prev_cam[2]);
   const double de = sqrt(radd(radd(rmul(dx, dx), rmul(dy, dy)), rmul(dz, dz)));
-  const float4 ndp = ld4(A.prev.nd, sp);
   if (!(fabs(rsub((double)ndp.w, de)) < rmul(C.depth_rel_tol, fmax(de, 1e-12)))) return;
   const double ndot = radd(radd(rmul((double)ndp.x, (double)nd.x), rmul((double)ndp.y, (double)nd.y)),
                            rmul((double)ndp.z, (double)nd.z));
   if (!(ndot > C.normal_dot_min)) return;
-  const int64_t gi = (int64_t)(sy - A.gin.row0) * C.width + sx;
-  float4 p0 = ld4(A.gin.g0, gi);
-  const float4 p1 = ld4(A.gin.g1, gi);
   if (C.rotate_mean) {
     bool keep;
     float ox, oy;
@@ -214,7 +216,9 @@ PGG_COLD bool accept_d(const CholD& cd, float mx, float my, uint32_t a, uint32_t
   return qx >= 0.0 && qx <= 1.0 && qy >= 0.0 && qy <= 1.0;
 }
 
-PGG_HD bool near_edge(float v) { return fabsf(v) < 1e-5f || fabsf(1.0f - v) < 1e-5f; }
+// float32 p = mu + L z carries <= ~1e-6 absolute error (|L z| <= 2): re-decide
+// within 3e-6 of an edge
+PGG_HD bool near_edge(float v) { return fabsf(v) < 3e-6f || fabsf(1.0f - v) < 3e-6f; }
 
 PGG_COLD V3<float> brdf_draw_local_d(const Mat<float>& mf, float alpha, const V3<float>& wol, bool co_pos,
                                      uint32_t a, uint32_t b, bool& ok) {
@@ -714,12 +718,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   const int64_t ci = (int64_t)(y - A.cur.row0) * W + x;
   const uint8_t fl = ldu8(A.cur.flags, ci);
   const bool valid = fl & 1;
-  float4 nd = f4(0, 0, 1, 0), pr = f4(0, 0, 0, 0), am = f4(0, 0, 0, 0);
-  if (valid) {
-    nd = ld4(A.cur.nd, ci);
-    pr = ld4(A.cur.pr, ci);
-    am = ld4(A.cur.am, ci);
-  }
+  // all own-pixel loads in flight together (invalid pixels are ~10 %)
+  const float4 nd = ld4(A.cur.nd, ci);
+  const float4 pr = ld4(A.cur.pr, ci);
+  const float4 am = ld4(A.cur.am, ci);
+  const float4 va = ld4(A.cur.va, ci);
   if (A.has_prev) {
     reproject_px(A, x, y, fl, nd, pr, am, g0, g1);
   } else {
@@ -744,7 +747,6 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     return false;
   }
   const LobeF L = make_lobe(g0.x, g0.y, g0.z, g0.w, g1.x, g1.z);
-  const float4 va = ld4(A.cur.va, ci);
   const V3<float> n = v3(nd.x, nd.y, nd.z);
   const V3<float> wo = v3(va.x, va.y, va.z);
   const float rough = pr.w;
@@ -822,6 +824,48 @@ PGG_HD void em_dump(const PassArgs& A, int x, int y, uint64_t s0, const uint64_t
     out[4 * s + 2] = o.w;
     out[4 * s + 3] = 1.0f;
   }
+}
+
+// EM context rebuilt by the split EM kernel from the G-buffer planes, the
+// reprojected Gamma and the lobe constants stage 1 stored (il11', l21',
+// il22', gnorm): the same floats the fused path keeps in registers.
+// Returns the train flag (valid pixel, view above the surface).
+PGG_HD bool em_setup_from_planes(const PassArgs& A, int x, int y, const float4& g0, const float4& g1,
+                                 const float4& lobe4, EmSetup& S) {
+  const pgg_config& C = A.cfg;
+  const int64_t ci = (int64_t)(y - A.cur.row0) * C.width + x;
+  const uint8_t fl = ldu8(A.cur.flags, ci);
+  S.flags = 0;
+  S.nb = 0;
+  if (!(fl & 1)) return false;
+  const float4 nd = ld4(A.cur.nd, ci), pr = ld4(A.cur.pr, ci), va = ld4(A.cur.va, ci), am = ld4(A.cur.am, ci);
+  const V3<float> n = v3(nd.x, nd.y, nd.z);
+  const PixelFrame pf = make_pixel_frame(n, v3(va.x, va.y, va.z));
+  if (!pf.co_pos) return false;
+  const bool glossy = (fl & 4) != 0;
+  const double r2d = (double)pr.w * (double)pr.w;
+  const float alpha = (float)fmax(r2d, 1e-6);
+  S.x = v3(pr.x, pr.y, pr.z);
+  S.fr = pf.fr;
+  S.n_raw = n;
+  S.wol = pf.wol;
+  S.alb_r = va.w;
+  S.alb_g = am.x;
+  S.alb_b = am.y;
+  S.a2 = alpha * alpha;
+  S.kappa = kappa_world(pf.om_nn, S.a2);
+  S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
+  S.mx = g0.x;
+  S.my = g0.y;
+  S.il11 = lobe4.x;
+  S.l21 = lobe4.y;
+  S.il22 = lobe4.z;
+  S.gnorm = lobe4.w;
+  S.pi = g1.z;
+  S.flags = 1 | (glossy ? 2 : 0) | 4;
+  S.nb = neighbor_budget(g1.w, C.k_max);
+  S.s0 = pcg_lane(C.key_train, (uint64_t)y * (uint64_t)C.width + (uint64_t)x);
+  return true;
 }
 
 // Whole pixel on one thread (host build): the device splits stage 2 over a
