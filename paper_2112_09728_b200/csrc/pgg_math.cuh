@@ -743,90 +743,96 @@ PGG_COLD float trunc_mass_f(float mx, float my, float l11, float l21, float l22)
   return fminf(fmaxf(acc, 1e-4f), 1.0f);
 }
 
-// Gauss-Legendre nodes (on [0,1]) and weights (for [-1,1]) of the BVN form
-#define PGG_GLN4(X) \
-  X(0.069431844202973714f, 0.34785484513745357f) \
-  X(0.33000947820757187f, 0.65214515486254643f) \
-  X(0.66999052179242813f, 0.65214515486254643f) \
-  X(0.93056815579702623f, 0.34785484513745357f)
-
-#define PGG_GLN6(X) \
-  X(0.03376524289842403f, 0.17132449237917027f) \
-  X(0.16939530676686776f, 0.36076157304813872f) \
-  X(0.38069040695840156f, 0.46791393457269104f) \
-  X(0.61930959304159849f, 0.46791393457269104f) \
-  X(0.83060469323313224f, 0.36076157304813872f) \
-  X(0.96623475710157591f, 0.17132449237917027f)
-
-#define PGG_GLN10(X) \
-  X(0.013046735741414128f, 0.066671344308688138f) \
-  X(0.067468316655507732f, 0.14945134915058039f) \
-  X(0.16029521585048778f, 0.21908636251598201f) \
-  X(0.28330230293537639f, 0.26926671930999652f) \
-  X(0.42556283050918442f, 0.29552422471475281f) \
-  X(0.57443716949081558f, 0.29552422471475281f) \
-  X(0.71669769706462361f, 0.26926671930999652f) \
-  X(0.83970478414951222f, 0.21908636251598201f) \
-  X(0.93253168334449232f, 0.14945134915058039f) \
-  X(0.98695326425858587f, 0.066671344308688138f)
-
-#define PGG_GLN12(X) \
-  X(0.0092196828766403782f, 0.047175336386511411f) \
-  X(0.047941371814762601f, 0.10693932599531907f) \
-  X(0.11504866290284765f, 0.16007832854334642f) \
-  X(0.20634102285669126f, 0.20316742672306573f) \
-  X(0.31608425050090994f, 0.23349253653835461f) \
-  X(0.43738329574426554f, 0.24914704581340269f) \
-  X(0.5626167042557344f, 0.24914704581340269f) \
-  X(0.68391574949909006f, 0.23349253653835461f) \
-  X(0.79365897714330869f, 0.20316742672306573f) \
-  X(0.88495133709715235f, 0.16007832854334642f) \
-  X(0.95205862818523745f, 0.10693932599531907f) \
-  X(0.99078031712335957f, 0.047175336386511411f)
-
-#define PGG_GLN16(X) \
-  X(0.0052995325041750307f, 0.027152459411754176f) \
-  X(0.0277124884633837f, 0.062253523938647456f) \
-  X(0.067184398806084122f, 0.095158511682492605f) \
-  X(0.1222977958224985f, 0.12462897125553407f) \
-  X(0.19106187779867811f, 0.14959598881657671f) \
-  X(0.27099161117138632f, 0.16915651939500265f) \
-  X(0.35919822461037054f, 0.18260341504492364f) \
-  X(0.45249374508118129f, 0.18945061045506864f) \
-  X(0.54750625491881877f, 0.18945061045506864f) \
-  X(0.64080177538962946f, 0.18260341504492364f) \
-  X(0.72900838882861363f, 0.16915651939500265f) \
-  X(0.80893812220132189f, 0.14959598881657671f) \
-  X(0.87770220417750155f, 0.12462897125553407f) \
-  X(0.93281560119391593f, 0.095158511682492605f) \
-  X(0.9722875115366163f, 0.062253523938647456f) \
-  X(0.99470046749582497f, 0.027152459411754176f)
-
-#define PGG_GLN24(X) \
-  X(0.0024063900014893447f, 0.01234122979998869f) \
-  X(0.012635722014345263f, 0.028531388628933559f) \
-  X(0.030862723998633601f, 0.044277438817419412f) \
-  X(0.056792236497799464f, 0.05929858491543636f) \
-  X(0.089999007013048526f, 0.073346481411080161f) \
-  X(0.12993790421072282f, 0.086190161531953205f) \
-  X(0.17595317403151223f, 0.097618652104113926f) \
-  X(0.22728926430558022f, 0.10744427011596556f) \
-  X(0.28310324618697746f, 0.11550566805372552f) \
-  X(0.3424786601519183f, 0.12167047292780329f) \
-  X(0.40444056626319186f, 0.12583745634682825f) \
-  X(0.46797155356869719f, 0.12793819534675202f) \
-  X(0.53202844643130276f, 0.12793819534675202f) \
-  X(0.5955594337368082f, 0.12583745634682825f) \
-  X(0.6575213398480817f, 0.12167047292780329f) \
-  X(0.71689675381302254f, 0.11550566805372552f) \
-  X(0.77271073569441984f, 0.10744427011596556f) \
-  X(0.82404682596848777f, 0.097618652104113926f) \
-  X(0.87006209578927718f, 0.086190161531953205f) \
-  X(0.91000099298695147f, 0.073346481411080161f) \
-  X(0.94320776350220048f, 0.05929858491543636f) \
-  X(0.96913727600136634f, 0.044277438817419412f) \
-  X(0.98736427798565474f, 0.028531388628933559f) \
-  X(0.99759360999851066f, 0.01234122979998869f)
+// Gauss-Legendre node sets of the BVN form, concatenated: n = 4, 6, 10, 12,
+// 16, 24 at offsets 0, 4, 10, 20, 32, 48 (nodes on [0,1], weights for [-1,1])
+#ifdef __CUDACC__
+__constant__ float c_glb_u[72] = {0.069431844202973714f, 0.33000947820757187f, 0.66999052179242813f, 0.93056815579702623f,
+    0.03376524289842403f, 0.16939530676686776f, 0.38069040695840156f, 0.61930959304159849f,
+    0.83060469323313224f, 0.96623475710157591f, 0.013046735741414128f, 0.067468316655507732f,
+    0.16029521585048778f, 0.28330230293537639f, 0.42556283050918442f, 0.57443716949081558f,
+    0.71669769706462361f, 0.83970478414951222f, 0.93253168334449232f, 0.98695326425858587f,
+    0.0092196828766403782f, 0.047941371814762601f, 0.11504866290284765f, 0.20634102285669126f,
+    0.31608425050090994f, 0.43738329574426554f, 0.5626167042557344f, 0.68391574949909006f,
+    0.79365897714330869f, 0.88495133709715235f, 0.95205862818523745f, 0.99078031712335957f,
+    0.0052995325041750307f, 0.0277124884633837f, 0.067184398806084122f, 0.1222977958224985f,
+    0.19106187779867811f, 0.27099161117138632f, 0.35919822461037054f, 0.45249374508118129f,
+    0.54750625491881877f, 0.64080177538962946f, 0.72900838882861363f, 0.80893812220132189f,
+    0.87770220417750155f, 0.93281560119391593f, 0.9722875115366163f, 0.99470046749582497f,
+    0.0024063900014893447f, 0.012635722014345263f, 0.030862723998633601f, 0.056792236497799464f,
+    0.089999007013048526f, 0.12993790421072282f, 0.17595317403151223f, 0.22728926430558022f,
+    0.28310324618697746f, 0.3424786601519183f, 0.40444056626319186f, 0.46797155356869719f,
+    0.53202844643130276f, 0.5955594337368082f, 0.6575213398480817f, 0.71689675381302254f,
+    0.77271073569441984f, 0.82404682596848777f, 0.87006209578927718f, 0.91000099298695147f,
+    0.94320776350220048f, 0.96913727600136634f, 0.98736427798565474f, 0.99759360999851066f};
+__constant__ float c_glb_w[72] = {0.34785484513745357f, 0.65214515486254643f, 0.65214515486254643f, 0.34785484513745357f,
+    0.17132449237917027f, 0.36076157304813872f, 0.46791393457269104f, 0.46791393457269104f,
+    0.36076157304813872f, 0.17132449237917027f, 0.066671344308688138f, 0.14945134915058039f,
+    0.21908636251598201f, 0.26926671930999652f, 0.29552422471475281f, 0.29552422471475281f,
+    0.26926671930999652f, 0.21908636251598201f, 0.14945134915058039f, 0.066671344308688138f,
+    0.047175336386511411f, 0.10693932599531907f, 0.16007832854334642f, 0.20316742672306573f,
+    0.23349253653835461f, 0.24914704581340269f, 0.24914704581340269f, 0.23349253653835461f,
+    0.20316742672306573f, 0.16007832854334642f, 0.10693932599531907f, 0.047175336386511411f,
+    0.027152459411754176f, 0.062253523938647456f, 0.095158511682492605f, 0.12462897125553407f,
+    0.14959598881657671f, 0.16915651939500265f, 0.18260341504492364f, 0.18945061045506864f,
+    0.18945061045506864f, 0.18260341504492364f, 0.16915651939500265f, 0.14959598881657671f,
+    0.12462897125553407f, 0.095158511682492605f, 0.062253523938647456f, 0.027152459411754176f,
+    0.01234122979998869f, 0.028531388628933559f, 0.044277438817419412f, 0.05929858491543636f,
+    0.073346481411080161f, 0.086190161531953205f, 0.097618652104113926f, 0.10744427011596556f,
+    0.11550566805372552f, 0.12167047292780329f, 0.12583745634682825f, 0.12793819534675202f,
+    0.12793819534675202f, 0.12583745634682825f, 0.12167047292780329f, 0.11550566805372552f,
+    0.10744427011596556f, 0.097618652104113926f, 0.086190161531953205f, 0.073346481411080161f,
+    0.05929858491543636f, 0.044277438817419412f, 0.028531388628933559f, 0.01234122979998869f};
+#endif
+static const float h_glb_u[72] = {0.069431844202973714f, 0.33000947820757187f, 0.66999052179242813f, 0.93056815579702623f,
+    0.03376524289842403f, 0.16939530676686776f, 0.38069040695840156f, 0.61930959304159849f,
+    0.83060469323313224f, 0.96623475710157591f, 0.013046735741414128f, 0.067468316655507732f,
+    0.16029521585048778f, 0.28330230293537639f, 0.42556283050918442f, 0.57443716949081558f,
+    0.71669769706462361f, 0.83970478414951222f, 0.93253168334449232f, 0.98695326425858587f,
+    0.0092196828766403782f, 0.047941371814762601f, 0.11504866290284765f, 0.20634102285669126f,
+    0.31608425050090994f, 0.43738329574426554f, 0.5626167042557344f, 0.68391574949909006f,
+    0.79365897714330869f, 0.88495133709715235f, 0.95205862818523745f, 0.99078031712335957f,
+    0.0052995325041750307f, 0.0277124884633837f, 0.067184398806084122f, 0.1222977958224985f,
+    0.19106187779867811f, 0.27099161117138632f, 0.35919822461037054f, 0.45249374508118129f,
+    0.54750625491881877f, 0.64080177538962946f, 0.72900838882861363f, 0.80893812220132189f,
+    0.87770220417750155f, 0.93281560119391593f, 0.9722875115366163f, 0.99470046749582497f,
+    0.0024063900014893447f, 0.012635722014345263f, 0.030862723998633601f, 0.056792236497799464f,
+    0.089999007013048526f, 0.12993790421072282f, 0.17595317403151223f, 0.22728926430558022f,
+    0.28310324618697746f, 0.3424786601519183f, 0.40444056626319186f, 0.46797155356869719f,
+    0.53202844643130276f, 0.5955594337368082f, 0.6575213398480817f, 0.71689675381302254f,
+    0.77271073569441984f, 0.82404682596848777f, 0.87006209578927718f, 0.91000099298695147f,
+    0.94320776350220048f, 0.96913727600136634f, 0.98736427798565474f, 0.99759360999851066f};
+static const float h_glb_w[72] = {0.34785484513745357f, 0.65214515486254643f, 0.65214515486254643f, 0.34785484513745357f,
+    0.17132449237917027f, 0.36076157304813872f, 0.46791393457269104f, 0.46791393457269104f,
+    0.36076157304813872f, 0.17132449237917027f, 0.066671344308688138f, 0.14945134915058039f,
+    0.21908636251598201f, 0.26926671930999652f, 0.29552422471475281f, 0.29552422471475281f,
+    0.26926671930999652f, 0.21908636251598201f, 0.14945134915058039f, 0.066671344308688138f,
+    0.047175336386511411f, 0.10693932599531907f, 0.16007832854334642f, 0.20316742672306573f,
+    0.23349253653835461f, 0.24914704581340269f, 0.24914704581340269f, 0.23349253653835461f,
+    0.20316742672306573f, 0.16007832854334642f, 0.10693932599531907f, 0.047175336386511411f,
+    0.027152459411754176f, 0.062253523938647456f, 0.095158511682492605f, 0.12462897125553407f,
+    0.14959598881657671f, 0.16915651939500265f, 0.18260341504492364f, 0.18945061045506864f,
+    0.18945061045506864f, 0.18260341504492364f, 0.16915651939500265f, 0.14959598881657671f,
+    0.12462897125553407f, 0.095158511682492605f, 0.062253523938647456f, 0.027152459411754176f,
+    0.01234122979998869f, 0.028531388628933559f, 0.044277438817419412f, 0.05929858491543636f,
+    0.073346481411080161f, 0.086190161531953205f, 0.097618652104113926f, 0.10744427011596556f,
+    0.11550566805372552f, 0.12167047292780329f, 0.12583745634682825f, 0.12793819534675202f,
+    0.12793819534675202f, 0.12583745634682825f, 0.12167047292780329f, 0.11550566805372552f,
+    0.10744427011596556f, 0.097618652104113926f, 0.086190161531953205f, 0.073346481411080161f,
+    0.05929858491543636f, 0.044277438817419412f, 0.028531388628933559f, 0.01234122979998869f};
+PGG_HD float glb_u(int i) {
+#ifdef __CUDA_ARCH__
+  return c_glb_u[i];
+#else
+  return h_glb_u[i];
+#endif
+}
+PGG_HD float glb_w(int i) {
+#ifdef __CUDA_ARCH__
+  return c_glb_w[i];
+#else
+  return h_glb_w[i];
+#endif
+}
 
 // Truncation mass as an exact bivariate-normal rectangle probability
 // (Genz 2004, "Numerical computation of rectangular bivariate and trivariate
@@ -857,29 +863,20 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
       const float hk1 = b1 * a2, hs1 = 0.5f * (b1 * b1 + a2 * a2);
       const float hk2 = a1 * b2, hs2 = 0.5f * (a1 * a1 + b2 * b2);
       const float hk3 = b1 * b2, hs3 = 0.5f * (b1 * b1 + b2 * b2);
+      // node count per |r| for float32 accuracy (measured); one
+      // loop over a constant table keeps the code small (icache)
+      const int cls = ar < 0.3f ? 0 : ar < 0.75f ? 1 : ar < 0.925f ? 2 : ar < 0.96f ? 3 : ar < 0.99f ? 4 : 5;
+      const int off = cls == 0 ? 0 : cls == 1 ? 4 : cls == 2 ? 10 : cls == 3 ? 20 : cls == 4 ? 32 : 48;
+      const int cnt = cls == 0 ? 4 : cls == 1 ? 6 : cls == 2 ? 10 : cls == 3 ? 12 : cls == 4 ? 16 : 24;
       float acc = 0.0f;
-#define PGG_X(un, wn)                                                                       \
-  {                                                                                         \
-    const float sn = f_sin(asr * (un));                                                     \
-    const float inv = f_div(1.0f, 1.0f - sn * sn);                                          \
-    const float e = f_exp((sn * hk0 - hs0) * inv) - f_exp((sn * hk1 - hs1) * inv) -          \
-                    f_exp((sn * hk2 - hs2) * inv) + f_exp((sn * hk3 - hs3) * inv);           \
-    acc = fmaf(wn, e, acc);                                                                 \
-  }
-      if (ar < 0.3f) {
-        PGG_GLN4(PGG_X)
-      } else if (ar < 0.75f) {
-        PGG_GLN6(PGG_X)
-      } else if (ar < 0.925f) {
-        PGG_GLN10(PGG_X)
-      } else if (ar < 0.96f) {
-        PGG_GLN12(PGG_X)
-      } else if (ar < 0.99f) {
-        PGG_GLN16(PGG_X)
-      } else {
-        PGG_GLN24(PGG_X)
+#pragma unroll 2
+      for (int i = off; i < off + cnt; ++i) {
+        const float sn = f_sin(asr * glb_u(i));
+        const float inv = f_rcp(1.0f - sn * sn);
+        const float e = f_exp((sn * hk0 - hs0) * inv) - f_exp((sn * hk1 - hs1) * inv) -
+                        f_exp((sn * hk2 - hs2) * inv) + f_exp((sn * hk3 - hs3) * inv);
+        acc = fmaf(glb_w(i), e, acc);
       }
-#undef PGG_X
       z += acc * asr * 0.079577471545947667884f;  // 1/(4 pi)
     }
   }
