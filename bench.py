@@ -31,6 +31,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 W, H, SEQ = 1920, 1080, 16
+WORKLOADS = {  # BASELINE.json configs
+    "1080p": (1920, 1080, 1, "configs[1]: 1920x1080 1 spp 16-frame sequence"),
+    "4k4spp": (3840, 2160, 4, "configs[3]: 3840x2160 4 spp guiding pass"),
+    "8k": (7680, 4320, 1, "configs[4]: 7680x4320 1 spp sequence"),
+}
 BYTES_PER_PX = 184          # fused pass, 1 spp
 BYTES_PER_EXTRA_SPP = 17
 
@@ -41,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=160)
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--spp", type=int, default=1)
+    ap.add_argument("--spp", type=int, default=None)
+    ap.add_argument("--workload", default="1080p", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -190,6 +196,76 @@ def bench_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def bench_bands(args, rank, world, local_rank):
+    """configs[3]/[4] at N GPUs: one frame split into N row bands, NCCL halo
+    exchange of the EM / reprojection halos every frame (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.bands import BandedGuiding
+    from paper_2112_09728_b200.layout import GBufferPlanes, PassConfig, VplPlanes
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = PassConfig(seed=0, spp=args.spp)
+    band = BandedGuiding(W, H, cfg, rank=rank, world=world, device=dev, max_motion_rows=8)
+    eg, ev = band.ext_g, band.ext_v
+    frames = []
+    for g, v in synth.sequence(W, H, SEQ, seed=0, device=dev):
+        full_g, full_v = GBufferPlanes.from_ref(g, device=dev), VplPlanes.from_ref(v, device=dev)
+        gb, vp = band.extended_planes()
+        for name in ("flags", "nd", "pr", "va", "am"):
+            eg.own(getattr(gb, name)).copy_(getattr(full_g, name)[band.r0:band.r1])
+        gb.cam_origin = full_g.cam_origin
+        ev.own(vp.y).copy_(full_v.y[band.r0:band.r1])
+        ev.own(vp.L).copy_(full_v.L[band.r0:band.r1])
+        frames.append((gb, vp))
+        del full_g, full_v
+    torch.cuda.synchronize(dev)
+    stream = torch.cuda.current_stream(dev)
+    state = {"i": 0}
+
+    def step():
+        i = state["i"]
+        gb, vp = frames[i % SEQ]
+        band.step(i % SEQ, gbuf=gb, vpl=vp)
+        state["i"] = i + 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        h0 = time.monotonic()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        clk.mark(h0, time.monotonic())
+    total = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms = float(total.item()) / args.steps
+    if rank == 0:
+        peak, peak_kind = peaks()
+        bpx = BYTES_PER_PX + BYTES_PER_EXTRA_SPP * (args.spp - 1)
+        achieved = bpx * W * H / (ms * 1e-3) / 1e9 / world
+        line = {"metric": f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)", "value": W * H / (ms * 1e-3) / 1e6,
+                "unit": "Mpixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOADS[args.workload][3] + ", row bands + NCCL halo exchange",
+                           "parallelism": f"bands{world}"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                             "note": "per GPU, step time incl. halo exchange"},
+                "clocks": clk.summary(), "gpu_launches": args.steps, "e2e": None, "cpu_baseline": None,
+                "halo_misses": band.halo_misses()}
+        print(json.dumps(line), flush=True)
+
+
 def bench_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -260,12 +336,15 @@ def bench_ours(args, rank, world, local_rank):
                "sample": f"one 1920x160 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
                          f"sampling + training_pass, oracle port of pgtrace on 1 core"}
     if rank == 0:
-        line = {"metric": "guiding-pass Mpixels/s at 1080p", "value": mpix, "unit": "Mpixels/s", "n_gpus": world,
+        metric = ("guiding-pass Mpixels/s at 1080p" if args.workload == "1080p"
+                  else f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)")
+        line = {"metric": metric, "value": mpix, "unit": "Mpixels/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_frame": ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
-                "config": {"workload": "1920x1080 %d spp 16-frame sequence, fused reproject+sample/pdf(MIS)+EM per "
-                                       "frame (BASELINE configs[1]); N>1 = N independent 1080p streams" % args.spp,
+                "config": {"workload": "%dx%d %d spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM "
+                                       "per frame (BASELINE %s); N>1 = N independent streams"
+                                       % (W, H, args.spp, WORKLOADS[args.workload][3].split(":")[0]),
                            "l2": "inputs larger than L2 (~200 MB/frame, 16 frames rotating); no flush",
                            "parallelism": "replicas" if world > 1 else "single"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -368,7 +447,11 @@ def bench_e2e(args, frames, cfg, dev, world):
 
 
 def main():
+    global W, H
     args = parse()
+    W, H, spp0, _ = WORKLOADS[args.workload]
+    if args.spp is None:
+        args.spp = spp0
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -381,7 +464,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
     __graft_entry__.build()
-    bench_ours(args, rank, world, local_rank)
+    if world > 1 and args.workload != "1080p":
+        bench_bands(args, rank, world, local_rank)
+    else:
+        bench_ours(args, rank, world, local_rank)
     if world > 1:
         dist.destroy_process_group()
 

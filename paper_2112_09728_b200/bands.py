@@ -114,40 +114,59 @@ class BandedGuiding:
         self.samples = SamplePlanes.empty(r1 - r0, width, cfg.spp, self.dev)
         self.cur = 0
         self.has_prev = False
+        self.prev_gb = None
         self._miss = torch.zeros(1, dtype=torch.int32, device=self.dev)
 
     def frame_inputs(self):
         """(G-buffer planes, VPL planes) whose OWN rows the caller fills."""
         return self.gb[self.cur], self.vpl
 
-    def halo_tensors(self):
+    def extended_planes(self):
+        """Fresh (G-buffer, VPL) planes with this band's extents, for callers
+        that keep one set per frame and pass them to step()."""
+        from .layout import GBufferPlanes, VplPlanes
+        eg, ev = self.ext_g, self.ext_v
+        gb = GBufferPlanes.empty(eg.rows, self.W, self.dev, row0=eg.lo)
+        vp = VplPlanes(torch.zeros(ev.rows, self.W, 4, device=self.dev),
+                       torch.zeros(ev.rows, self.W, 4, device=self.dev), row0=ev.lo)
+        return gb, vp
+
+    def halo_tensors(self, vpl=None):
         """The (extent, tensors) pairs whose halo rows step() exchanges."""
-        prev = self.gb[1 - self.cur]
+        vpl = vpl if vpl is not None else self.vpl
+        prev = self.prev_gb
         g_in = self.gamma[self.cur]
-        pairs = [(self.ext_v, [self.vpl.y, self.vpl.L])]
+        pairs = [(self.ext_v, [vpl.y, vpl.L])]
         if self.has_prev:
             pairs.append((self.ext_g, [prev.flags, prev.nd, g_in.g0, g_in.g1]))
         return pairs
 
-    def step(self, frame, exchange=True):
+    def step(self, frame, exchange=True, gbuf=None, vpl=None):
         """Exchange halos (unless the caller already filled them, exchange=False)
-        and run the fused pass on this band."""
+        and run the fused pass on this band.  ``gbuf``/``vpl``: this frame's
+        extended planes (own rows filled); default: the internal buffers."""
         from .session import run_pass
-        cur, prev = self.gb[self.cur], self.gb[1 - self.cur]
+        if gbuf is None:
+            cur = self.gb[self.cur]
+        else:
+            cur = gbuf
+        vpl = vpl if vpl is not None else self.vpl
+        prev = self.prev_gb
         g_in, g_out = self.gamma[self.cur], self.gamma[1 - self.cur]
         if exchange:
             # halos: this frame's VPLs; previous frame's Gamma and gate planes
-            for tag, (ext, ts) in enumerate(self.halo_tensors()):
+            for tag, (ext, ts) in enumerate(self.halo_tensors(vpl)):
                 halo_exchange(ts, ext, self.rank, self.world, self.group, tag=1 + tag)
         eg = self.ext_g
         out_view = type(g_out)(eg.own(g_out.g0), eg.own(g_out.g1), row0=self.r0)
         cur_band = type(cur)(eg.own(cur.flags), eg.own(cur.nd), eg.own(cur.pr), eg.own(cur.va), eg.own(cur.am),
                              cur.cam_origin, row0=self.r0)
-        res = run_pass(self.cfg, frame, cur_band, g_in, prev=prev if self.has_prev else None, vpl=self.vpl,
+        res = run_pass(self.cfg, frame, cur_band, g_in, prev=prev if self.has_prev else None, vpl=vpl,
                        height=self.H, row0=self.r0, rows=self.r1 - self.r0, out_gamma=out_view,
                        out_samples=self.samples, halo_misses=self._miss)
         self.cur = 1 - self.cur
         self.has_prev = True
+        self.prev_gb = cur
         return res
 
     @property
