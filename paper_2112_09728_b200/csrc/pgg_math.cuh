@@ -362,9 +362,9 @@ template <class T> PGG_HD V3<T> sq_to_dir(T px, T py) {
 // Inverse lift + inverse concentric map, clipped to [0,1]^2.  Callers pass
 // z >= 0 (the reference raises below -1e-9; sgmap.py:72-73).
 template <class T> PGG_HD void dir_to_sq(const V3<T>& v, T& sx, T& sy) {
-  const T s = m_sqrt(m_max(T(1) + v.z, T(1e-30)));
-  const T x = v.x / s;
-  const T y = v.y / s;
+  const T is = T(1) / m_sqrt(m_max(T(1) + v.z, T(1e-30)));
+  const T x = v.x * is;
+  const T y = v.y * is;
   const T rho = m_sqrt(x * x + y * y);
   T a, b;
   if (rho == T(0)) {
@@ -846,18 +846,20 @@ PGG_HD float glb_w(int i) {
 // typically); |r| >= 0.999 falls back to the reference rule itself.
 PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double sxy, float l11, float l21,
                             float l22) {
-  const double sx = sqrt(sxx), sy = sqrt(syy);
-  const double rd = sxy / (sx * sy);
-  const float ar = (float)fabs(rd);
+  // standardised bounds and correlation in float32 (the result is float32;
+  // float64 here bought nothing but DP divisions)
+  const float mxf = (float)mx, myf = (float)my;
+  const float isx = r_rsqrt((float)sxx), isy = r_rsqrt((float)syy);
+  const float r = (float)sxy * isx * isy;
+  const float ar = fabsf(r);
   float z;
   if (ar >= 0.999f) {
-    z = trunc_mass_f((float)mx, (float)my, l11, l21, l22);
+    z = trunc_mass_f(mxf, myf, l11, l21, l22);
   } else {
-    const float a1 = (float)((0.0 - mx) / sx), b1 = (float)((1.0 - mx) / sx);
-    const float a2 = (float)((0.0 - my) / sy), b2 = (float)((1.0 - my) / sy);
+    const float a1 = (0.0f - mxf) * isx, b1 = (1.0f - mxf) * isx;
+    const float a2 = (0.0f - myf) * isy, b2 = (1.0f - myf) * isy;
     z = ndtr_diff(b1, a1) * ndtr_diff(b2, a2);
-    if (rd != 0.0) {
-      const float r = (float)rd;
+    if (sxy != 0.0) {
       const float asr = asinf(r);
       const float hk0 = a1 * a2, hs0 = 0.5f * (a1 * a1 + a2 * a2);
       const float hk1 = b1 * a2, hs1 = 0.5f * (b1 * b1 + a2 * a2);
@@ -911,10 +913,11 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
   L.l11 = (float)l11;
   L.l21 = (float)l21;
   L.l22 = (float)l22;
-  L.il11 = (float)(1.0 / l11);
-  L.il22 = (float)(1.0 / l22);
+  L.il11 = 1.0f / L.l11;
+  L.il22 = 1.0f / L.l22;
   L.z = trunc_mass_bvn(mx, my, sxx, syy, sxy, L.l11, L.l21, L.l22);
-  L.gnorm = (float)(1.0 / (2.0 * K<double>::pi * l11 * l22) / (double)L.z * K<double>::inv_2pi);
+  // 1 / (2 pi l11 l22 Z) / (2 pi)
+  L.gnorm = L.il11 * L.il22 * (0.025330295910584444f / L.z);
   L.pi = pi;
   L.reset = reset ? 1 : 0;
   return L;
