@@ -23,6 +23,13 @@
  *   pgg_frame_key ........ the lane-independent prefix of rng.make_streams
  *   pgg_pack_* / pgg_gamma_* layout conversion at the API edge
  *
+ * The render pass that feeds it:
+ *   pgg_gbuffer_pass ..... ptrace.gbuffer_pass          ptrace.py:97-129
+ *                          ptrace.motion_vectors        ptrace.py:132-150
+ *   pgg_render_pass ...... ptrace.render_frame / _render_chunk / _trace_lanes
+ *                          ptrace.py:223-355, 382-586 (scene.intersect,
+ *                          occluded, sample_emitter, brdf_* scene.py:158-414)
+ *
  * Conventions: every pointer is a DEVICE pointer owned by the caller unless
  * stated otherwise; calls are asynchronous on `stream` (a cudaStream_t, NULL =
  * legacy default stream), keep no global mutable state, never throw, and
@@ -32,13 +39,16 @@
  * Device layouts (P = pixels of a row band, row-major, width = frame width):
  *   Gamma      two float4 planes  g0 = (mu_x, mu_y, m2_xx, m2_yy)
  *                                 g1 = (m2_xy, w_sum, pi, k)
- *   G-buffer   flags u8 (bit0 valid, bit1 has_history, bit2 glossy)
+ *   G-buffer   flags u8 (bit0 valid, bit1 has_history, bit2 glossy, bit3 front)
  *              nd float4 (normal.xyz, depth)      pr float4 (pos.xyz, roughness)
  *              va float4 (view.xyz, albedo.r)     am float4 (albedo.g, albedo.b, motion.xy)
+ *              mat int32 plane (material id, -1 on a miss; render pass only)
  *   VPLs (Pi)  y float4 (pos.xyz, usable = valid && strategy==BRDF ? 1 : 0)
- *              L float4 (radiance.rgb, 0)
+ *              L float4 (radiance.rgb, valid | strategy << 1)
  *   samples    per lane (pixel*spp + s): dir float4 (wi.xyz world, pdf),
- *              tag u8 (bit0 strategy GAUSSIAN, bit1 valid)
+ *              tag u8 (bit0 strategy GAUSSIAN, bit1 valid, bits 2..7 the
+ *              number of PCG32 draws the depth-0 sampler consumed after the
+ *              NEE draws, so the render pass continues the lane's stream)
  */
 #ifndef PGG_H_
 #define PGG_H_
@@ -50,7 +60,7 @@
 extern "C" {
 #endif
 
-#define PGG_ABI_VERSION 1
+#define PGG_ABI_VERSION 2
 
 enum pgg_status {
   PGG_OK = 0,
@@ -186,6 +196,57 @@ int pgg_gamma_split(int64_t p, const float* aos, float* g0, float* g1, void* str
 int pgg_gamma_join(int64_t p, const float* g0, const float* g1, float* aos, void* stream);
 /* Fresh Gamma (mixture.init_stats) into the planes. */
 int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Render pass (the producer of the G-buffer and the VPLs). */
+
+/* Scene table (device, float64; built by paper_2112_09728_b200/scene.py
+ * Scene.pack): n_mat x 8 (kind, albedo rgb, roughness, emission rgb),
+ * n_sph x 8 (center xyz, radius, material, pad), n_quad x 16 (corner, edge_u,
+ * edge_v, unit normal, area, material, |edge_u|^2, |edge_v|^2), n_emit
+ * emitter quad indices.  At most 6144 doubles (staged in shared memory). */
+typedef struct pgg_scene {
+  const double* table;
+  int32_t n_mat, n_sph, n_quad, n_emit;
+  double background[3];
+} pgg_scene;
+
+/* Pinhole camera of one frame (scene.camera_at, scene.py:94-117). */
+typedef struct pgg_camera {
+  double origin[3], forward[3], right[3], up[3];
+  double tan_half_fov;
+} pgg_camera;
+
+/* Primary hit per pixel centre of rows [row0, row0 + rows) into the packed
+ * G-buffer planes (+ material ids); prev_cam != NULL also writes the motion
+ * vectors and has_history of motion_vectors(prev_cam, cam, gbuf). */
+int pgg_gbuffer_pass(const pgg_scene* scene, const pgg_camera* cam, const pgg_camera* prev_cam, int32_t width,
+                     int32_t height, int32_t row0, int32_t rows, uint8_t* flags, float* nd, float* pr, float* va,
+                     float* am, int32_t* mat, void* stream);
+
+typedef struct pgg_render_config {
+  int32_t width, height;       /* full frame */
+  int32_t row0, rows;          /* band rendered by this call */
+  int32_t spp, max_depth, nee; /* PathConfig (ptrace.py:27-40) */
+  int32_t reserved;
+  uint64_t key;                /* pgg_frame_key(seed, frame, 0) */
+} pgg_render_config;
+
+typedef struct pgg_render_out {
+  float* image;                   /* rows x W x 3, mean over spp */
+  float* vpl_y;                   /* VPL planes of the band (layout above) */
+  float* vpl_L;
+  double* lum_moments;            /* rows x W x 2 (sum, sum of squares of luminance) or NULL */
+  unsigned long long* counters;   /* [scatter segments, non-finite samples] accumulated, or NULL */
+} pgg_render_out;
+
+/* Trace spp lanes per pixel from the G-buffer (gb + mat planes holding the
+ * band): NEE at every vertex, BRDF scatter, VPL of the last lane.  depth0 !=
+ * NULL (pg mode): the depth-0 scatter of every lane comes from the guiding
+ * pass's samples of the same band and frame (pgg_guiding_pass with
+ * nee_draws = nee && n_emit ? 3 : 0). */
+int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const pgg_gbuffer* gb, const int32_t* mat,
+                    const pgg_samples* depth0, const pgg_render_out* out, void* stream);
 
 const char* pgg_status_string(int status);
 const char* pgg_last_cuda_error(void);

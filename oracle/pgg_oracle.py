@@ -93,6 +93,19 @@ def draw_u32(state):
     return (xs >> rot) | (xs << ((np.uint32(32) - rot) & np.uint32(31)))
 
 
+def lcg_distance(a, b, limit=64):
+    """Number of LCG steps from states a to states b (< limit), per lane."""
+    cur = np.array(a, dtype=np.uint64, copy=True)
+    n = np.full(cur.shape, -1, dtype=np.int64)
+    n[cur == b] = 0
+    for i in range(1, limit):
+        with np.errstate(over="ignore"):
+            cur = cur * PCG_MUL + PCG_ADD
+        n[(n < 0) & (cur == b)] = i
+    assert np.all(n >= 0), "state not reachable within the limit"
+    return n
+
+
 def draw_unit(state):
     """u32 * 2^-32 as float64, exact (pg/rng.py:53-55)."""
     return draw_u32(state).astype(np.float64) * (2.0 ** -32)
@@ -204,7 +217,7 @@ def brdf_value(kind, albedo, rough, wi, wo, n):
         h = unit(wi + wo)
         ch = np.abs(dot3(h, n))
         hi = dot3(h, wi)
-        spec = (_ndf(alpha, ch) * _g1(alpha, np.abs(ci)) * _g1(alpha, np.abs(co))
+        spec = (_ndf(alpha, ch) * (_g1(alpha, np.abs(ci)) * _g1(alpha, np.abs(co)))
                 / np.maximum(4.0 * ci * co, 1e-30))
         fres = albedo + (1.0 - albedo) * np.power(np.clip(1.0 - np.abs(hi), 0.0, 1.0), 5.0)[..., None]
         f = np.where((gl & up)[..., None], fres * spec[..., None], f)
@@ -606,7 +619,8 @@ def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROU
     valid & (diffuse | rough >= rough_min) & k >= 1.
 
     Returns dict with wi (P,spp,3), pdf (P,spp), strategy (P,spp) uint8,
-    valid (P,spp) bool; invalid pixels are all zero."""
+    valid (P,spp) bool, draws (P,spp) = PCG32 draws the sampler consumed
+    after the NEE draws; invalid pixels are all zero."""
     h, w = stats_f32.shape[:2]
     p = h * w
     st = stats_f32.reshape(-1, 8).astype(np.float64)
@@ -625,11 +639,14 @@ def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROU
     nrm = gbuf.normal.reshape(-1, 3)[pix]
     wo = gbuf.view.reshape(-1, 3)[pix]
     lbp = SimpleNamespace(mu=lb.mu[pix], l11=lb.l11[pix], l21=lb.l21[pix], l22=lb.l22[pix], z=lb.z[pix])
+    out["draws"] = np.zeros((p, spp), dtype=np.int64)
     for s in range(spp):
         state = seed_lanes(seed, frame, pix.astype(np.uint64) * np.uint64(spp) + np.uint64(s), 0)
         for _ in range(nee_draws):
             draw_u32(state)
+        start = state.copy()
         wi, pdf, strat, ok = first_bounce(pos, nrm, kind[pix], rough[pix], wo, st[pix], lbp, guided[pix], state)
+        out["draws"][pix, s] = lcg_distance(start, state)
         out["wi"][pix, s] = wi
         out["pdf"][pix, s] = pdf
         out["strategy"][pix, s] = strat

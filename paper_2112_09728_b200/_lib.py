@@ -54,6 +54,25 @@ class Config(ctypes.Structure):
                 ("prev_cam", c_f64 * 3), ("key_sample", c_u64), ("key_train", c_u64)]
 
 
+class Scene(ctypes.Structure):
+    _fields_ = [("table", c_p), ("n_mat", c_i32), ("n_sph", c_i32), ("n_quad", c_i32), ("n_emit", c_i32),
+                ("background", c_f64 * 3)]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("origin", c_f64 * 3), ("forward", c_f64 * 3), ("right", c_f64 * 3), ("up", c_f64 * 3),
+                ("tan_half_fov", c_f64)]
+
+
+class RenderConfig(ctypes.Structure):
+    _fields_ = [("width", c_i32), ("height", c_i32), ("row0", c_i32), ("rows", c_i32), ("spp", c_i32),
+                ("max_depth", c_i32), ("nee", c_i32), ("reserved", c_i32), ("key", c_u64)]
+
+
+class RenderOut(ctypes.Structure):
+    _fields_ = [("image", c_p), ("vpl_y", c_p), ("vpl_L", c_p), ("lum_moments", c_p), ("counters", c_p)]
+
+
 _SIGS = {
     "pgg_guiding_pass": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GBuffer),
                          ctypes.POINTER(GammaIn), ctypes.POINTER(Vpl), ctypes.POINTER(GammaOut),
@@ -71,6 +90,10 @@ _SIGS = {
     "pgg_gamma_split": [c_i64, c_p, c_p, c_p, c_p],
     "pgg_gamma_join": [c_i64, c_p, c_p, c_p, c_p],
     "pgg_gamma_init": [c_i64, c_p, c_p, c_p],
+    "pgg_gbuffer_pass": [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.POINTER(Camera), c_i32, c_i32, c_i32,
+                         c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "pgg_render_pass": [ctypes.POINTER(RenderConfig), ctypes.POINTER(Scene), ctypes.POINTER(GBuffer), c_p,
+                        ctypes.POINTER(Samples), ctypes.POINTER(RenderOut), c_p],
 }
 
 EXPORTS = tuple(_SIGS) + ("pgg_frame_key", "pgg_status_string", "pgg_last_cuda_error", "pgg_abi_version")

@@ -51,15 +51,14 @@ class Extent:
         return t[self.r0 - self.lo:self.r1 - self.lo]
 
 
-def halo_exchange(tensors, ext, rank, world, group=None, tag=0):
-    """Fill the halo rows of the extended tensors (each (ext.rows, W, ...))
-    from the neighbouring bands: rank-1 sends its last rows, rank+1 its first.
-
-    Ranks agree on the halo depth, so the rows rank r needs from rank r+1 are
-    exactly the rows rank r+1 sends up.  One grouped batch of P2P ops."""
-    if world == 1:
-        return
+def halo_ops(tensors, ext, rank, world, group=None, tag=0):
+    """The P2P ops that fill the halo rows of the extended tensors (each
+    (ext.rows, W, ...)) from the neighbouring bands: rank-1 sends its last
+    rows, rank+1 its first.  Ranks agree on the halo depth, so the rows rank r
+    needs from rank r+1 are exactly the rows rank r+1 sends up."""
     ops = []
+    if world == 1:
+        return ops
     up_rows = ext.r0 - ext.lo       # rows [lo, r0) come from rank - 1
     down_rows = ext.hi - ext.r1     # rows [r1, hi) come from rank + 1
     for t in tensors:
@@ -70,9 +69,20 @@ def halo_exchange(tensors, ext, rank, world, group=None, tag=0):
         if rank < world - 1 and down_rows > 0:
             ops.append(dist.P2POp(dist.isend, own[own.shape[0] - down_rows:].contiguous(), rank + 1, group, tag))
             ops.append(dist.P2POp(dist.irecv, t[t.shape[0] - down_rows:], rank + 1, group, tag))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    return ops
+
+
+def post_exchange(ops):
+    """Issue one grouped batch of P2P ops; returns the requests (wait() on
+    each before reading the halos; on NCCL the wait orders the current CUDA
+    stream after the transfer without blocking the host)."""
+    return dist.batch_isend_irecv(ops) if ops else []
+
+
+def halo_exchange(tensors, ext, rank, world, group=None, tag=0):
+    """Blocking halo fill of the extended tensors (one grouped batch)."""
+    for req in post_exchange(halo_ops(tensors, ext, rank, world, group, tag)):
+        req.wait()
 
 
 def check_band_geometry(height, world, halo):
@@ -141,33 +151,69 @@ class BandedGuiding:
             pairs.append((self.ext_g, [prev.flags, prev.nd, g_in.g0, g_in.g1]))
         return pairs
 
-    def step(self, frame, exchange=True, gbuf=None, vpl=None):
+    def split_rows(self):
+        """(interior, edges): the interior rows of the band read no halo row
+        (every read is within max(R, M) rows of the pixel), so they can run
+        while the halo exchange is in flight; edges are the rows next to a
+        neighbouring band.  Every pixel's result is independent of how the
+        band is split into launches (bitwise)."""
+        h = max(self.R, self.M)
+        lo = self.r0 + (h if self.rank > 0 else 0)
+        hi = self.r1 - (h if self.rank < self.world - 1 else 0)
+        if hi <= lo:
+            return None, [(self.r0, self.r1)]
+        edges = [(a, b) for a, b in ((self.r0, lo), (hi, self.r1)) if b > a]
+        return (lo, hi), edges
+
+    def _launch(self, frame, a, b, cur_band, vpl, prev, g_in, g_out):
+        from .layout import SamplePlanes
+        from .session import run_pass
+        eg = self.ext_g
+        out_view = type(g_out)(g_out.g0[a - eg.lo:b - eg.lo], g_out.g1[a - eg.lo:b - eg.lo], row0=a)
+        smp = SamplePlanes(self.samples.dir[a - self.r0:b - self.r0], self.samples.tag[a - self.r0:b - self.r0],
+                           self.samples.spp)
+        return run_pass(self.cfg, frame, cur_band, g_in, prev=prev if self.has_prev else None, vpl=vpl,
+                        height=self.H, row0=a, rows=b - a, out_gamma=out_view, out_samples=smp,
+                        halo_misses=self._miss)
+
+    def step(self, frame, exchange=True, gbuf=None, vpl=None, overlap=True, split=None):
         """Exchange halos (unless the caller already filled them, exchange=False)
         and run the fused pass on this band.  ``gbuf``/``vpl``: this frame's
-        extended planes (own rows filled); default: the internal buffers."""
-        from .session import run_pass
-        if gbuf is None:
-            cur = self.gb[self.cur]
-        else:
-            cur = gbuf
+        extended planes (own rows filled); default: the internal buffers.
+
+        overlap=True: the grouped send/recv is posted first, the
+        interior rows run while it is in flight, and the edge rows after the
+        stream has waited on it; overlap=False runs exchange, then one launch.
+        split=True/False forces the interior/edge launches on or off."""
+        from .session import PassResult
+        cur = self.gb[self.cur] if gbuf is None else gbuf
         vpl = vpl if vpl is not None else self.vpl
         prev = self.prev_gb
         g_in, g_out = self.gamma[self.cur], self.gamma[1 - self.cur]
-        if exchange:
-            # halos: this frame's VPLs; previous frame's Gamma and gate planes
-            for tag, (ext, ts) in enumerate(self.halo_tensors(vpl)):
-                halo_exchange(ts, ext, self.rank, self.world, self.group, tag=1 + tag)
         eg = self.ext_g
-        out_view = type(g_out)(eg.own(g_out.g0), eg.own(g_out.g1), row0=self.r0)
         cur_band = type(cur)(eg.own(cur.flags), eg.own(cur.nd), eg.own(cur.pr), eg.own(cur.va), eg.own(cur.am),
                              cur.cam_origin, row0=self.r0)
-        res = run_pass(self.cfg, frame, cur_band, g_in, prev=prev if self.has_prev else None, vpl=vpl,
-                       height=self.H, row0=self.r0, rows=self.r1 - self.r0, out_gamma=out_view,
-                       out_samples=self.samples, halo_misses=self._miss)
+        reqs = []
+        if exchange and self.world > 1:
+            # halos: this frame's VPLs; previous frame's Gamma and gate planes
+            ops = []
+            for tag, (ext, ts) in enumerate(self.halo_tensors(vpl)):
+                ops += halo_ops(ts, ext, self.rank, self.world, self.group, tag=1 + tag)
+            reqs = post_exchange(ops)
+        if split is None:
+            split = overlap and bool(reqs)
+        interior, edges = self.split_rows() if split else (None, [(self.r0, self.r1)])
+        if interior is not None:
+            self._launch(frame, *interior, cur_band, vpl, prev, g_in, g_out)
+        for req in reqs:
+            req.wait()
+        for a, b in edges:
+            self._launch(frame, a, b, cur_band, vpl, prev, g_in, g_out)
         self.cur = 1 - self.cur
         self.has_prev = True
         self.prev_gb = cur
-        return res
+        from .layout import GammaPlanes
+        return PassResult(gamma=GammaPlanes(eg.own(g_out.g0), eg.own(g_out.g1), row0=self.r0), samples=self.samples)
 
     @property
     def gamma_own(self):

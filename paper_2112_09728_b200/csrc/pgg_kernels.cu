@@ -16,8 +16,8 @@
 
 using namespace pgg;
 
-namespace {
-
+// shared with the render translation unit (pgg_render.cu)
+namespace pgg_rt {
 thread_local char g_cuda_err[256] = "";
 
 int check_launch() {
@@ -28,6 +28,12 @@ int check_launch() {
   }
   return PGG_OK;
 }
+}  // namespace pgg_rt
+
+namespace {
+
+using pgg_rt::check_launch;
+using pgg_rt::g_cuda_err;
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -187,6 +187,7 @@ struct LaneOut {
   float pdf;
   int gauss;
   int valid;
+  int draws;  // PCG32 draws consumed (the render continues the stream after them)
 };
 
 // float64 Cholesky provider for the rare guard-band acceptance recheck
@@ -259,14 +260,17 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
     o.pdf = co_pos ? brdf_pdf_local(mf, wl, wol) : 0.0f;
     o.gauss = 0;
     o.valid = ok && o.pdf > 0.0f;
+    o.draws = 2;
     return o;
   }
   const uint32_t uz = pcg_next(st);
+  o.draws = 1;
   bool acc = false;
   float sx = 0.0f, sy = 0.0f;
   if (u01d(uz) < (double)L.pi) {
     for (int t = 0; t < GAUSS_TRIES; ++t) {
       const uint32_t a = pcg_next(st), b = pcg_next(st);
+      o.draws += 2;
       float z0, z1;
       box_muller_f(a, b, z0, z1);
       const float px = L.mx + L.l11 * z0;
@@ -291,6 +295,7 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
     dl = sq_to_dir<float>(sx, sy);
   } else {
     const uint32_t a = pcg_next(st), b = pcg_next(st);
+    o.draws += 2;
     dl = brdf_draw_local(mf, alpha, wol, co_pos, a, b, ok);
   }
   o.gauss = acc ? 1 : 0;
@@ -622,6 +627,14 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   if (s >= S.nb) return;
   sa = jmul[s - 1] * S.s0 + jadd[s - 1];
   sb = jmul[s + 18] * S.s0 + jadd[s + 18];
+#ifndef PGG_EM_UNROLL
+#define PGG_EM_UNROLL 1
+#endif
+#if PGG_EM_UNROLL == 2
+#pragma unroll 2
+#elif PGG_EM_UNROLL == 3
+#pragma unroll 3
+#endif
   for (; s < S.nb; s += EM_LANES) {
     const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
     sa = sa * JL_MUL + JL_ADD;
@@ -767,7 +780,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
       for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
       const LaneOut o = sample_lane(pf, glossy, rough, guided, L, cd, st);
       st4(A.smp.dir, own * C.spp + s, f4(o.wi.x, o.wi.y, o.wi.z, o.pdf));
-      A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1));
+      A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
     }
   }
   if (!A.has_vpl) return false;

@@ -1,0 +1,611 @@
+// pgg_render.cu — the render pass that produces the guiding pass's inputs
+// (SURVEY.md 8f rank 1): primary-ray G-buffer + camera motion vectors
+// (pg/ptrace.py:97-150) and the path-traced lanes with next-event estimation
+// that write the image and the per-pixel VPLs (pg/ptrace.py:223-355,
+// 382-586; scene routines pg/scene.py:158-241, 247-414).
+//
+// Precision: the reference traces in float64 and its hit / visibility
+// decisions are discontinuous, so this translation unit computes geometry,
+// BRDFs and throughput in float64 with the reference's operation order and
+// is compiled with -fmad=false (no contraction): primary rays, NEE and
+// scatter decisions match the reference's bit for bit except where NumPy's
+// BLAS dot products or libm transcendentals round differently (1 ulp).
+// B200 runs FP64 at half the FP32 rate; the scene is a few dozen
+// primitives held in shared memory, so a lane is latency- not bandwidth-
+// bound (render pass).
+//
+// Lanes: one thread per pixel walks its spp lanes in order (lane key
+// pixel * spp + s, pg/ptrace.py:474), so the per-pixel sums accumulate in the
+// reference's order.  In pg mode the depth-0 scatter comes from the guiding
+// pass's samples (pgg_guiding_pass, samples != NULL) and the lane's PCG32
+// stream continues after the draws that sampler consumed (tag bits 2..7).
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "pgg.h"
+
+namespace pgg_rt {
+extern thread_local char g_cuda_err[256];
+int check_launch();
+}  // namespace pgg_rt
+
+namespace {
+
+// PCG32 lane streams (pg/rng.py:10-55; same chain as pgg_math.cuh)
+constexpr uint64_t PCG_MUL = 6364136223846793005ULL;
+constexpr uint64_t PCG_INC = 1442695040888963407ULL;
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t pcg_lane(uint64_t key, uint64_t lane) {
+  return mix64(key ^ mix64(lane)) * PCG_MUL + PCG_INC;
+}
+__device__ __forceinline__ uint32_t pcg_next(uint64_t& s) {
+  const uint64_t old = s;
+  s = old * PCG_MUL + PCG_INC;
+  const uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+  const uint32_t rot = (uint32_t)(old >> 59);
+  return (xs >> rot) | (xs << ((32u - rot) & 31u));
+}
+__device__ __forceinline__ double u01d(uint32_t u) { return (double)u * 2.3283064365386963e-10; }
+
+constexpr double PI_D = 3.141592653589793;
+constexpr double RAY_EPS = 1e-4;  // pg/scene.py:24
+constexpr int MAT_STRIDE = 8, SPH_STRIDE = 8, QUAD_STRIDE = 16;  // scene.py pack()
+constexpr int MAX_TABLE = 6144;   // doubles staged in shared memory (48 KB)
+
+struct D3 {
+  double x, y, z;
+};
+__device__ __forceinline__ D3 d3(double x, double y, double z) { return {x, y, z}; }
+__device__ __forceinline__ D3 operator+(D3 a, D3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ D3 operator-(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ D3 operator*(D3 a, D3 b) { return {a.x * b.x, a.y * b.y, a.z * b.z}; }
+__device__ __forceinline__ D3 operator*(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ D3 operator*(double s, D3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ D3 operator/(D3 a, double s) { return {a.x / s, a.y / s, a.z / s}; }
+__device__ __forceinline__ D3 neg(D3 a) { return {-a.x, -a.y, -a.z}; }
+// np.sum(a * b, axis=-1): sequential over the three products
+__device__ __forceinline__ double dot(D3 a, D3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__device__ __forceinline__ double norm(D3 a) { return sqrt(dot(a, a)); }
+// pg/scene.py:31-34
+__device__ __forceinline__ D3 normalize(D3 a) { return a / fmax(norm(a), 1e-30); }
+__device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ bool any_pos(D3 a) { return a.x > 0.0 || a.y > 0.0 || a.z > 0.0; }
+__device__ __forceinline__ bool finite3(D3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+__device__ __forceinline__ D3 ld3(const double* p) { return {p[0], p[1], p[2]}; }
+
+// Scene table staged in shared memory (layout: paper_2112_09728_b200/scene.py)
+struct SceneS {
+  const double* mats;
+  const double* sph;
+  const double* quad;
+  const double* emit;
+  int nm, ns, nq, ne;
+  D3 bg;
+  __device__ int kind(int m) const { return (int)mats[m * MAT_STRIDE]; }
+  __device__ D3 albedo(int m) const { return ld3(mats + m * MAT_STRIDE + 1); }
+  __device__ double rough(int m) const { return mats[m * MAT_STRIDE + 4]; }
+  __device__ D3 emission(int m) const { return ld3(mats + m * MAT_STRIDE + 5); }
+};
+
+__device__ SceneS stage_scene(const pgg_scene& sc, double* smem) {
+  const int n = sc.n_mat * MAT_STRIDE + sc.n_sph * SPH_STRIDE + sc.n_quad * QUAD_STRIDE + sc.n_emit;
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  for (int i = tid; i < n; i += blockDim.x * blockDim.y) smem[i] = sc.table[i];
+  __syncthreads();
+  SceneS s;
+  s.mats = smem;
+  s.sph = s.mats + sc.n_mat * MAT_STRIDE;
+  s.quad = s.sph + sc.n_sph * SPH_STRIDE;
+  s.emit = s.quad + sc.n_quad * QUAD_STRIDE;
+  s.nm = sc.n_mat;
+  s.ns = sc.n_sph;
+  s.nq = sc.n_quad;
+  s.ne = sc.n_emit;
+  s.bg = d3(sc.background[0], sc.background[1], sc.background[2]);
+  return s;
+}
+
+struct Hit {
+  bool hit, front;
+  double t;
+  D3 pos, nrm;
+  int mat;
+};
+
+// Nearest hit, spheres then quads, strict t < best (pg/scene.py:158-235).
+// any_hit: stop at the first primitive inside (t_min, t_max) (occluded()).
+template <bool kAny>
+__device__ Hit cast(const SceneS& S, D3 o, D3 d, double t_min, double t_max) {
+  double best = INFINITY;
+  int which = -1, prim = -1;
+  for (int i = 0; i < S.ns; ++i) {
+    const double* sp = S.sph + i * SPH_STRIDE;
+    const D3 oc = o - ld3(sp);
+    const double r = sp[3];
+    const double b = dot(oc, d);
+    const double c = dot(oc, oc) - r * r;
+    const double disc = b * b - c;
+    bool ok = disc > 0.0;
+    const double root = sqrt(ok ? disc : 0.0);
+    const double t0 = -b - root, t1 = -b + root;
+    const double t = (t0 > t_min && t0 < t_max) ? t0 : t1;
+    ok = ok && t > t_min && t < t_max && t < best;
+    if (ok) {
+      best = t;
+      which = 0;
+      prim = i;
+      if (kAny) break;
+    }
+  }
+  if (!kAny || which < 0) {
+    for (int i = 0; i < S.nq; ++i) {
+      const double* q = S.quad + i * QUAD_STRIDE;
+      const D3 qn = ld3(q + 9);
+      const double den = dot(d, qn);
+      bool ok = fabs(den) > 1e-12;
+      const D3 corner = ld3(q);
+      const double t = ok ? dot(corner - o, qn) / den : INFINITY;
+      const D3 rel = (o + d * t) - corner;
+      const double u = dot(rel, ld3(q + 3)) / q[14];
+      const double v = dot(rel, ld3(q + 6)) / q[15];
+      ok = ok && u >= 0.0 && u <= 1.0 && v >= 0.0 && v <= 1.0;
+      ok = ok && t > t_min && t < t_max && t < best;
+      if (ok) {
+        best = t;
+        which = 1;
+        prim = i;
+        if (kAny) break;
+      }
+    }
+  }
+  Hit h;
+  h.hit = which >= 0;
+  h.t = best;
+  if (kAny || !h.hit) {
+    h.front = false;
+    h.mat = -1;
+    return h;
+  }
+  h.pos = o + d * best;
+  if (which == 0) {
+    const double* sp = S.sph + prim * SPH_STRIDE;
+    h.nrm = (h.pos - ld3(sp)) / sp[3];
+    h.mat = (int)sp[4];
+  } else {
+    const double* q = S.quad + prim * QUAD_STRIDE;
+    h.nrm = ld3(q + 9);
+    h.mat = (int)q[13];
+  }
+  const double facing = dot(h.nrm, d);
+  h.front = facing < 0.0;
+  if (facing > 0.0) h.nrm = neg(h.nrm);
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// BRDFs in float64 (pg/scene.py:247-380), NumPy operation order
+
+__device__ __forceinline__ double ggx_ndf(double alpha, double c) {
+  const double a2 = alpha * alpha;
+  const double d = c * c * (a2 - 1.0) + 1.0;
+  return a2 / fmax(PI_D * d * d, 1e-30);
+}
+__device__ __forceinline__ double smith_g1(double alpha, double c) {
+  const double a2 = alpha * alpha;
+  return 2.0 * c / fmax(c + sqrt(a2 + (1.0 - a2) * c * c), 1e-30);
+}
+
+__device__ D3 brdf_eval(int kind, D3 alb, double rough, D3 wi, D3 wo, D3 n) {
+  const double ci = dot(wi, n), co = dot(wo, n);
+  if (!(ci > 0.0 && co > 0.0)) return d3(0, 0, 0);
+  if (kind != 1) return alb / PI_D;
+  const double alpha = fmax(rough * rough, 1e-6);
+  const D3 h = normalize(wi + wo);
+  const double ch = fabs(dot(h, n));
+  const double hw = dot(h, wi);
+  const double d = ggx_ndf(alpha, ch);
+  const double g = smith_g1(alpha, fabs(ci)) * smith_g1(alpha, fabs(co));
+  const double p5 = pow(fmin(fmax(1.0 - fabs(hw), 0.0), 1.0), 5.0);
+  const double sc = d * g / fmax(4.0 * ci * co, 1e-30);
+  const D3 fres = alb + (d3(1, 1, 1) - alb) * p5;
+  return fres * sc;
+}
+
+__device__ double brdf_pdf(int kind, double rough, D3 wi, D3 wo, D3 n) {
+  const double ci = dot(wi, n), co = dot(wo, n);
+  if (!(ci > 0.0 && co > 0.0)) return 0.0;
+  if (kind != 1) return ci / PI_D;
+  const double alpha = fmax(rough * rough, 1e-6);
+  const D3 h = normalize(wi + wo);
+  const double ch = fabs(dot(h, n));
+  return smith_g1(alpha, fabs(co)) * ggx_ndf(alpha, ch) / fmax(4.0 * co, 1e-30);
+}
+
+// revised ONB keyed on sign(n_z) (pg/sgmap.py:85-98)
+struct Onb {
+  D3 t, b, n;
+  __device__ D3 world(D3 v) const { return (t * v.x + b * v.y) + n * v.z; }
+  __device__ D3 local(D3 v) const { return d3(dot(v, t), dot(v, b), dot(v, n)); }
+};
+__device__ Onb onb(D3 n) {
+  const double s = copysign(1.0, n.z);
+  const double a = -1.0 / (s + n.z);
+  const double b = n.x * n.y * a;
+  return {d3(1.0 + s * n.x * n.x * a, s * b, -s * n.x), d3(b, s + n.y * n.y * a, -n.y), n};
+}
+
+__device__ D3 vndf_local(double alpha, D3 wo_l, double u1, double u2) {
+  const D3 vh = normalize(wo_l * d3(alpha, alpha, 1.0));
+  const double lensq = vh.x * vh.x + vh.y * vh.y;
+  const bool safe = lensq > 1e-18;
+  const double inv = 1.0 / sqrt(safe ? lensq : 1.0);
+  const D3 t1 = safe ? d3(-vh.y * inv, vh.x * inv, 0.0) : d3(1.0, 0.0, 0.0);
+  const D3 t2 = cross(vh, t1);
+  const double r = sqrt(u1);
+  const double phi = 2.0 * PI_D * u2;
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  const double p1 = r * cp;
+  double p2 = r * sp;
+  const double s = 0.5 * (1.0 + vh.z);
+  p2 = (1.0 - s) * sqrt(fmax(1.0 - p1 * p1, 0.0)) + s * p2;
+  const D3 nh = (t1 * p1 + t2 * p2) + vh * sqrt(fmax(1.0 - p1 * p1 - p2 * p2, 0.0));
+  const D3 h = normalize(d3(alpha * nh.x, alpha * nh.y, fmax(nh.z, 1e-9)));
+  return (2.0 * dot(wo_l, h)) * h - wo_l;
+}
+
+// world-space BRDF sample, two draws (pg/scene.py:354-380)
+__device__ D3 brdf_sample(int kind, double rough, D3 wo, D3 n, uint64_t& st, double& pdf, bool& valid) {
+  const double u1 = u01d(pcg_next(st));
+  const double u2 = u01d(pcg_next(st));
+  const Onb f = onb(n);
+  D3 wl;
+  if (kind == 1) {
+    const double alpha = fmax(rough * rough, 1e-6);
+    wl = vndf_local(alpha, f.local(wo), u1, u2);
+  } else {
+    const double r = sqrt(u1);
+    const double ang = 2.0 * PI_D * u2;
+    double sa, ca;
+    sincos(ang, &sa, &ca);
+    wl = d3(r * ca, r * sa, sqrt(fmax(1.0 - u1, 0.0)));
+  }
+  const D3 wi = f.world(wl);
+  valid = dot(wi, n) > 1e-9 && dot(wo, n) > 0.0;
+  pdf = brdf_pdf(kind, rough, wi, wo, n);
+  valid = valid && pdf > 0.0;
+  return wi;
+}
+
+// NEE toward one uniformly picked one-sided quad emitter, three draws
+// (pg/scene.py:386-414)
+__device__ void sample_emitter(const SceneS& S, D3 p, uint64_t& st, D3& dir, double& dist, D3& le, double& pdf) {
+  const double up = u01d(pcg_next(st));
+  const double u1 = u01d(pcg_next(st));
+  const double u2 = u01d(pcg_next(st));
+  long long pick = (long long)(up * (double)S.ne);
+  if (pick > S.ne - 1) pick = S.ne - 1;
+  const int qi = (int)S.emit[pick];
+  const double* q = S.quad + qi * QUAD_STRIDE;
+  const D3 y = (ld3(q) + ld3(q + 3) * u1) + ld3(q + 6) * u2;
+  const D3 d = y - p;
+  dist = fmax(norm(d), 1e-12);
+  dir = d / dist;
+  const double cos_l = -dot(dir, ld3(q + 9));
+  const bool lit = cos_l > 1e-9;
+  pdf = lit ? dist * dist / (q[12] * fmax(cos_l, 1e-12) * (double)S.ne) : 0.0;
+  le = lit ? S.emission((int)q[13]) : d3(0, 0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// G-buffer kernel (pg/ptrace.py:97-150, pg/scene.py:125-151)
+
+struct GbArgs {
+  pgg_scene scene;
+  pgg_camera cam, prev;
+  int has_prev;
+  int W, H, row0, rows;
+  uint8_t* flags;
+  float4 *nd, *pr, *va, *am;
+  int32_t* mat;
+};
+
+__device__ __forceinline__ D3 cam3(const double* v) { return d3(v[0], v[1], v[2]); }
+
+__global__ void __launch_bounds__(128) k_gbuffer(const GbArgs A) {
+  extern __shared__ double smem[];
+  const SceneS S = stage_scene(A.scene, smem);
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int yl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= A.W || yl >= A.rows) return;
+  const int y = A.row0 + yl;
+  const int64_t o = (int64_t)yl * A.W + x;
+  const double aspect = (double)A.W / (double)A.H;
+  const double th = A.cam.tan_half_fov;
+  const double ndc_x = (2.0 * ((double)x + 0.5) / (double)A.W - 1.0) * th * aspect;
+  const double ndc_y = (1.0 - 2.0 * ((double)y + 0.5) / (double)A.H) * th;
+  const D3 d = normalize((cam3(A.cam.forward) + cam3(A.cam.right) * ndc_x) + cam3(A.cam.up) * ndc_y);
+  const Hit h = cast<false>(S, cam3(A.cam.origin), d, RAY_EPS, INFINITY);
+  const D3 view = neg(d);
+  if (!h.hit) {
+    A.flags[o] = 0;
+    A.nd[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    A.pr[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    A.va[o] = make_float4((float)view.x, (float)view.y, (float)view.z, 0.f);
+    A.am[o] = make_float4(0.f, 0.f, 0.f, 0.f);
+    A.mat[o] = -1;
+    return;
+  }
+  const int m = h.mat;
+  const D3 alb = S.albedo(m);
+  float mx = 0.f, my = 0.f;
+  bool has = false;
+  if (A.has_prev) {
+    // previous camera's projection of the hit (pg/scene.py:138-151, pg/ptrace.py:132-150)
+    const D3 dd = h.pos - cam3(A.prev.origin);
+    const double zc = dot(dd, cam3(A.prev.forward));
+    const bool in_front = zc > 1e-9;
+    const double z = in_front ? zc : 1.0;
+    const double xc = dot(dd, cam3(A.prev.right)) / z;
+    const double yc = dot(dd, cam3(A.prev.up)) / z;
+    const double pth = A.prev.tan_half_fov;
+    const double px = (xc / (pth * aspect) + 1.0) * 0.5 * (double)A.W - 0.5;
+    const double py = (1.0 - yc / pth) * 0.5 * (double)A.H - 0.5;
+    const double tx = rint(px), ty = rint(py);
+    has = in_front && tx >= 0.0 && tx < (double)A.W && ty >= 0.0 && ty < (double)A.H;
+    if (has) {
+      mx = (float)(px - (double)x);
+      my = (float)(py - (double)y);
+    }
+  }
+  const bool glossy = S.kind(m) == 1;
+  A.flags[o] = (uint8_t)(1 | (has ? 2 : 0) | (glossy ? 4 : 0) | (h.front ? 8 : 0));
+  A.nd[o] = make_float4((float)h.nrm.x, (float)h.nrm.y, (float)h.nrm.z, (float)h.t);
+  A.pr[o] = make_float4((float)h.pos.x, (float)h.pos.y, (float)h.pos.z, (float)S.rough(m));
+  A.va[o] = make_float4((float)view.x, (float)view.y, (float)view.z, (float)alb.x);
+  A.am[o] = make_float4((float)alb.y, (float)alb.z, mx, my);
+  A.mat[o] = m;
+}
+
+// ---------------------------------------------------------------------------
+// Path lanes (pg/ptrace.py:223-355) and the per-pixel accumulation of
+// pg/ptrace.py:382-494
+
+struct RenderArgs {
+  pgg_render_config cfg;
+  pgg_scene scene;
+  pgg_gbuffer gb;
+  const int32_t* mat;
+  const float4* s_dir;  // depth-0 samples (pg mode) or NULL
+  const uint8_t* s_tag;
+  pgg_render_out out;
+};
+
+struct LaneResult {
+  D3 L, Li, vy;
+  bool vv;
+  int vs;
+  int segs;
+};
+
+__device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool valid0, bool front0, D3 pos, D3 nrm,
+                                 int mat, D3 wo, uint64_t st, int64_t lane_own) {
+  const pgg_render_config& C = A.cfg;
+  LaneResult R;
+  R.L = d3(0, 0, 0);
+  R.Li = d3(0, 0, 0);
+  R.vy = d3(0, 0, 0);
+  R.vv = false;
+  R.vs = 0;
+  R.segs = 0;
+  if (!valid0) {
+    R.L = S.bg;
+    return R;
+  }
+  if (front0) R.L = R.L + S.emission(mat);
+  D3 T = d3(1, 1, 1), Tr = d3(0, 0, 0);
+  const bool do_nee = C.nee && S.ne > 0;
+  for (int depth = 0; depth < C.max_depth; ++depth) {
+    const int kd = S.kind(mat);
+    const D3 alb = S.albedo(mat);
+    const double rg = S.rough(mat);
+    if (do_nee) {
+      D3 ld, le;
+      double dist, lpdf;
+      sample_emitter(S, pos, st, ld, dist, le, lpdf);
+      const D3 f = brdf_eval(kd, alb, rg, ld, wo, nrm);
+      const double cx = dot(ld, nrm);
+      D3 c = d3(0, 0, 0);
+      if (lpdf > 0.0 && cx > 0.0 && any_pos(f)) {
+        if (!cast<true>(S, pos, ld, RAY_EPS, dist - RAY_EPS).hit) c = le * f * (cx / lpdf);
+      }
+      R.L = R.L + T * c;
+      if (depth >= 1) R.Li = R.Li + Tr * c;
+    }
+    D3 wi;
+    double pdf;
+    bool ok;
+    int strat = 0;
+    if (depth == 0 && A.s_dir) {
+      // guided (or plain) depth-0 sample of the guiding pass; continue the
+      // stream after the draws it consumed
+      const float4 sd = A.s_dir[lane_own];
+      const uint8_t tg = A.s_tag[lane_own];
+      wi = d3(sd.x, sd.y, sd.z);
+      pdf = (double)sd.w;
+      ok = (tg & 2) != 0;
+      strat = tg & 1;
+      for (int k = tg >> 2; k > 0; --k) st = st * PCG_MUL + PCG_INC;
+    } else {
+      wi = brdf_sample(kd, rg, wo, nrm, st, pdf, ok);
+    }
+    const D3 f = brdf_eval(kd, alb, rg, wi, wo, nrm);
+    const double ci = dot(wi, nrm);
+    ok = ok && pdf > 0.0 && ci > 0.0;
+    if (!ok) break;
+    const D3 w = f * (ci / pdf);
+    T = T * w;
+    if (depth >= 1) Tr = Tr * w;
+    if (depth == 0) R.vs = strat;
+    const Hit h = cast<false>(S, pos, wi, RAY_EPS, INFINITY);
+    ++R.segs;
+    if (!h.hit) {
+      R.L = R.L + T * S.bg;
+      if (depth >= 1) R.Li = R.Li + Tr * S.bg;
+      break;
+    }
+    pos = h.pos;
+    nrm = h.nrm;
+    mat = h.mat;
+    wo = neg(wi);
+    if (depth == 0) {
+      R.vv = true;
+      R.vy = h.pos;
+      Tr = d3(1, 1, 1);
+      if (h.front) R.Li = R.Li + S.emission(h.mat);
+    }
+  }
+  return R;
+}
+
+__global__ void __launch_bounds__(128) k_render(const RenderArgs A) {
+  extern __shared__ double smem[];
+  const SceneS S = stage_scene(A.scene, smem);
+  const pgg_render_config& C = A.cfg;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int yl = blockIdx.y * blockDim.y + threadIdx.y;
+  const bool in = x < C.width && yl < C.rows;
+  int segs = 0, bad = 0;
+  if (in) {
+    const int y = C.row0 + yl;
+    const int64_t own = (int64_t)yl * C.width + x;
+    const int64_t gi = (int64_t)(y - A.gb.row0) * C.width + x;
+    const uint8_t fl = A.gb.flags[gi];
+    const bool valid = fl & 1, front = (fl & 8) != 0;
+    const float4 nd = reinterpret_cast<const float4*>(A.gb.nd)[gi];
+    const float4 pr = reinterpret_cast<const float4*>(A.gb.pr)[gi];
+    const float4 va = reinterpret_cast<const float4*>(A.gb.va)[gi];
+    const int m = valid ? A.mat[gi] : 0;
+    const uint64_t pix = (uint64_t)y * (uint64_t)C.width + (uint64_t)x;
+    D3 acc = d3(0, 0, 0);
+    double lsum = 0.0, lsq = 0.0;
+    LaneResult R;
+    for (int s = 0; s < C.spp; ++s) {
+      const uint64_t st = pcg_lane(C.key, pix * (uint64_t)C.spp + (uint64_t)s);
+      R = trace_lane(A, S, valid, front, d3(pr.x, pr.y, pr.z), d3(nd.x, nd.y, nd.z), m, d3(va.x, va.y, va.z), st,
+                     own * C.spp + s);
+      segs += R.segs;
+      if (!finite3(R.L)) {
+        ++bad;
+        R.L = d3(0, 0, 0);
+      }
+      if (!finite3(R.Li)) {
+        R.Li = d3(0, 0, 0);
+        R.vv = false;
+      }
+      acc = acc + R.L;
+      const double lum = (R.L.x * 0.2126 + R.L.y * 0.7152) + R.L.z * 0.0722;
+      lsum += lum;
+      lsq += lum * lum;
+    }
+    const D3 img = acc / (double)C.spp;
+    float* im = A.out.image + own * 3;
+    im[0] = (float)img.x;
+    im[1] = (float)img.y;
+    im[2] = (float)img.z;
+    // VPL of the last lane, in the guiding pass's packed layout
+    const bool usable = R.vv && R.vs == 0;
+    reinterpret_cast<float4*>(A.out.vpl_y)[own] =
+        make_float4((float)R.vy.x, (float)R.vy.y, (float)R.vy.z, usable ? 1.0f : 0.0f);
+    reinterpret_cast<float4*>(A.out.vpl_L)[own] =
+        make_float4((float)R.Li.x, (float)R.Li.y, (float)R.Li.z, (float)((R.vv ? 1 : 0) | (R.vs << 1)));
+    if (A.out.lum_moments) {
+      A.out.lum_moments[2 * own] = lsum;
+      A.out.lum_moments[2 * own + 1] = lsq;
+    }
+  }
+  if (A.out.counters) {
+    const unsigned sg = __reduce_add_sync(0xffffffffu, (unsigned)segs);
+    const unsigned bd = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0) {
+      if (sg) atomicAdd(A.out.counters, (unsigned long long)sg);
+      if (bd) atomicAdd(A.out.counters + 1, (unsigned long long)bd);
+    }
+  }
+}
+
+int table_doubles(const pgg_scene* s) {
+  return s->n_mat * MAT_STRIDE + s->n_sph * SPH_STRIDE + s->n_quad * QUAD_STRIDE + s->n_emit;
+}
+
+bool scene_ok(const pgg_scene* s) {
+  return s && s->table && s->n_mat > 0 && s->n_sph >= 0 && s->n_quad >= 0 && s->n_emit >= 0 &&
+         s->n_emit <= s->n_quad && table_doubles(s) <= MAX_TABLE;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pgg_gbuffer_pass(const pgg_scene* scene, const pgg_camera* cam, const pgg_camera* prev_cam, int32_t width,
+                     int32_t height, int32_t row0, int32_t rows, uint8_t* flags, float* nd, float* pr, float* va,
+                     float* am, int32_t* mat, void* stream) {
+  if (!scene_ok(scene) || !cam || width <= 0 || height <= 0 || row0 < 0 || rows < 0 || row0 + rows > height ||
+      !flags || !nd || !pr || !va || !am || !mat)
+    return PGG_ERR_ARGUMENT;
+  if (rows == 0) return PGG_OK;
+  GbArgs A;
+  A.scene = *scene;
+  A.cam = *cam;
+  A.has_prev = prev_cam != nullptr;
+  if (prev_cam) A.prev = *prev_cam;
+  A.W = width;
+  A.H = height;
+  A.row0 = row0;
+  A.rows = rows;
+  A.flags = flags;
+  A.nd = reinterpret_cast<float4*>(nd);
+  A.pr = reinterpret_cast<float4*>(pr);
+  A.va = reinterpret_cast<float4*>(va);
+  A.am = reinterpret_cast<float4*>(am);
+  A.mat = mat;
+  const dim3 blk(32, 4), grd((width + 31) / 32, (rows + 3) / 4);
+  k_gbuffer<<<grd, blk, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  return pgg_rt::check_launch();
+}
+
+int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const pgg_gbuffer* gb, const int32_t* mat,
+                    const pgg_samples* depth0, const pgg_render_out* out, void* stream) {
+  if (!cfg || !scene_ok(scene) || !gb || !mat || !out || !out->image || !out->vpl_y || !out->vpl_L)
+    return PGG_ERR_ARGUMENT;
+  if (cfg->width <= 0 || cfg->height <= 0 || cfg->row0 < 0 || cfg->rows < 0 || cfg->row0 + cfg->rows > cfg->height ||
+      cfg->spp < 1 || cfg->max_depth < 1 || cfg->spp * 35 > (1 << 30))
+    return PGG_ERR_ARGUMENT;
+  if (gb->row0 > cfg->row0 || gb->row0 + gb->rows < cfg->row0 + cfg->rows || !gb->flags || !gb->nd || !gb->pr ||
+      !gb->va)
+    return PGG_ERR_ARGUMENT;
+  if (depth0 && (!depth0->dir || !depth0->tag)) return PGG_ERR_ARGUMENT;
+  if (cfg->rows == 0) return PGG_OK;
+  RenderArgs A;
+  A.cfg = *cfg;
+  A.scene = *scene;
+  A.gb = *gb;
+  A.mat = mat;
+  A.s_dir = depth0 ? reinterpret_cast<const float4*>(depth0->dir) : nullptr;
+  A.s_tag = depth0 ? depth0->tag : nullptr;
+  A.out = *out;
+  const dim3 blk(32, 4), grd((cfg->width + 31) / 32, (cfg->rows + 3) / 4);
+  k_render<<<grd, blk, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  return pgg_rt::check_launch();
+}
+
+}  // extern "C"

@@ -1,10 +1,10 @@
-"""Render-side types and the guided first-bounce sampler; drop-in for the
-parts of pgtrace.ptrace on the guiding path (pg/ptrace.py:27-73, 161-220).
+"""Drop-in for pgtrace.ptrace (pg/ptrace.py): render-side types, the
+guided first-bounce sampler (pg/ptrace.py:161-220) and the render pass that
+feeds the guiding pass -- gbuffer_pass, motion_vectors and render_frame
+(pg/ptrace.py:97-150, 382-586) -- on the GPU kernels of csrc/pgg_render.cu.
 
-The ray-traced render pass itself (gbuffer_pass, _trace_lanes, ...) is
-outside this framework's scope: a renderer hands over
-its G-buffer and VPL buffer in these types, or in the packed device layout
-of layout.py.
+These wrappers take and return the reference's NumPy types; the
+device-resident path (no host copies) is render.py + cli.RenderSession.
 """
 
 from dataclasses import dataclass, field
@@ -14,6 +14,7 @@ import numpy as np
 import torch
 
 from . import _conv, mixture
+from . import scene as sc
 from .layout import GammaPlanes, GBufferPlanes, PassConfig, SamplePlanes
 from .session import run_pass
 
@@ -123,3 +124,155 @@ def sample_first_bounce_frame(gamma_stats, gbuf, seed, frame_index, spp=1, nee_d
     if torch_in:
         return out
     return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+# ---------------------------------------------------------------------------
+# render pass (pg/ptrace.py:76-150, 382-586)
+
+@dataclass
+class RenderResult:
+    """(pg/ptrace.py:76-86)"""
+
+    image: np.ndarray
+    vpl: VplBuffer
+    gbuffer: GBuffer
+    mean_path_length: float
+    nonfinite_count: int
+    lum_mean: Optional[np.ndarray] = None
+    lum_var: Optional[np.ndarray] = None
+
+
+def _device_scene(scene):
+    from .render import DeviceScene
+    dev = _conv.device()
+    cached = getattr(scene, "_pgg_device_scene", None)
+    if cached is None or cached.device != dev:
+        cached = DeviceScene(scene, dev)
+        try:
+            scene._pgg_device_scene = cached
+        except AttributeError:
+            pass
+    return cached
+
+
+def gbuffer_from_planes(fgb, cam_origin):
+    """Packed device G-buffer -> reference GBuffer (float64 NumPy fields).
+    Invalid pixels carry the reference's values: pos = origin + inf * dir
+    (non-finite), zero normal/depth/material fields, mat -1."""
+    g = fgb.planes
+    h, w = g.rows, g.width
+    fl = g.flags.cpu().numpy()
+    nd = g.nd.cpu().numpy().astype(np.float64)
+    pr = g.pr.cpu().numpy().astype(np.float64)
+    va = g.va.cpu().numpy().astype(np.float64)
+    am = g.am.cpu().numpy().astype(np.float64)
+    valid = (fl & 1).astype(bool)
+    view = va[..., :3]
+    pos = pr[..., :3].copy()
+    with np.errstate(invalid="ignore", over="ignore"):
+        pos[~valid] = np.asarray(cam_origin, dtype=np.float64) + np.inf * (-view[~valid])
+    mat = fgb.mat.cpu().numpy().astype(np.int32)
+    return GBuffer(
+        width=w, height=h, valid=valid, pos=pos, normal=nd[..., :3].copy(), depth=nd[..., 3].copy(), mat=mat,
+        kind=((fl >> 2) & 1).astype(np.int32), albedo=np.stack([va[..., 3], am[..., 0], am[..., 1]], axis=-1),
+        roughness=pr[..., 3].copy(), front=((fl >> 3) & 1).astype(bool), view=view.copy(),
+        motion=np.stack([am[..., 2], am[..., 3]], axis=-1), has_history=((fl >> 1) & 1).astype(bool),
+        cam_origin=np.asarray(cam_origin, dtype=np.float64).copy())
+
+
+def gbuffer_pass(scene, frame_index, resolution):
+    """One primary ray through each pixel centre (pg/ptrace.py:97-129), on
+    the GPU; float32 fields upcast to float64 NumPy."""
+    from .render import gbuffer_planes
+    width, height = resolution
+    cam = sc.camera_at(scene, frame_index)
+    fgb = gbuffer_planes(_device_scene(scene), cam, int(width), int(height))
+    return gbuffer_from_planes(fgb, cam.origin)
+
+
+def motion_vectors(prev_cam, cur_cam, gbuf):
+    """Offsets to the previous camera's projection of every valid hit
+    (pg/ptrace.py:132-150; pg/scene.py:138-151), float64 on the device."""
+    dev = _conv.device()
+    h, w = gbuf.height, gbuf.width
+    f64 = torch.float64
+    pos = _conv.to_dev(gbuf.pos, f64).reshape(-1, 3)
+    t = lambda v: torch.as_tensor(np.asarray(v, dtype=np.float64), device=dev)  # noqa: E731
+    d = pos - t(prev_cam.origin)
+    zc = d @ t(prev_cam.forward)
+    front = zc > 1e-9
+    z = torch.where(front, zc, torch.ones_like(zc))
+    xc = (d @ t(prev_cam.right)) / z
+    yc = (d @ t(prev_cam.up)) / z
+    aspect = w / float(h)
+    px = ((xc / (prev_cam.tan_half_fov * aspect) + 1.0) * 0.5 * w - 0.5).reshape(h, w)
+    py = ((1.0 - yc / prev_cam.tan_half_fov) * 0.5 * h - 0.5).reshape(h, w)
+    ii, jj = torch.meshgrid(torch.arange(h, device=dev, dtype=f64), torch.arange(w, device=dev, dtype=f64),
+                            indexing="ij")
+    tx, ty = torch.round(px), torch.round(py)  # half-to-even like np.rint
+    valid = _conv.to_dev(gbuf.valid, torch.bool)
+    has = valid & front.reshape(h, w) & (tx >= 0) & (tx < w) & (ty >= 0) & (ty < h)
+    zero = torch.zeros_like(px)
+    m = torch.stack([torch.where(has, px - jj, zero), torch.where(has, py - ii, zero)], dim=-1)
+    if _conv.is_torch(gbuf.pos):
+        return m, has
+    return m.cpu().numpy(), has.cpu().numpy()
+
+
+def _planes_from_gbuffer(gbuf, dev):
+    """Reference GBuffer -> FrameGBuffer (packed planes + front bit + mat)."""
+    from .render import FrameGBuffer
+    planes = GBufferPlanes.from_ref(gbuf, device=dev)
+    front = _conv.to_dev(gbuf.front, torch.uint8)
+    planes.flags |= (front & 1) << 3
+    planes.height = int(gbuf.height)
+    mat = _conv.to_dev(gbuf.mat, torch.int32)
+    return FrameGBuffer(planes, mat)
+
+
+def render_frame(scene, frame_index, guiding_stats, cfg, seed, resolution=None, gbuf=None, want_moments=False):
+    """Render one frame on the GPU (pg/ptrace.py:496-586): pt mode traces
+    BRDF lanes; pg mode (cfg.guiding with stats) first runs the guiding
+    pass's depth-0 sampler on the Gamma, then traces from its samples."""
+    from .render import render_planes
+    if gbuf is None:
+        if resolution is None:
+            raise ValueError("render_frame needs either a G-buffer or a resolution")
+        gbuf = gbuffer_pass(scene, frame_index, resolution)
+    h, w = gbuf.height, gbuf.width
+    guided = bool(cfg.guiding and guiding_stats is not None)
+    if guided:
+        gs = guiding_stats
+        if (gs.numel() if torch.is_tensor(gs) else np.asarray(gs).size) != h * w * 8:
+            raise ValueError("guiding buffer dimensions do not match the resolution")
+    dev = _conv.device()
+    dsc = _device_scene(scene)
+    fgb = _planes_from_gbuffer(gbuf, dev)
+    depth0 = None
+    if guided:
+        stats = _conv.to_dev(guiding_stats, torch.float32).reshape(h, w, 8)
+        pc = PassConfig(seed=seed, spp=cfg.spp, nee_draws=3 if (cfg.nee and scene.num_emitters) else 0,
+                        roughness_min_guide=cfg.roughness_min_guide)
+        depth0 = run_pass(pc, frame_index, fgb.planes, GammaPlanes.from_aos(stats, dev), want_samples=True).samples
+    rp = render_planes(dsc, fgb, frame_index, seed, spp=cfg.spp, max_depth=cfg.max_depth, nee=cfg.nee,
+                       depth0=depth0, want_moments=want_moments)
+    return result_from_planes(rp, gbuf, cfg.spp, want_moments)
+
+
+def result_from_planes(rp, gbuf, spp, want_moments):
+    """RenderPlanes -> reference RenderResult (NumPy)."""
+    h, w = rp.image.shape[:2]
+    cnt = rp.counters.cpu().numpy()
+    vy = rp.vpl.y.cpu().numpy().astype(np.float64)
+    vl = rp.vpl.L.cpu().numpy()
+    code = vl[..., 3].astype(np.int32)
+    vpl = VplBuffer(valid=(code & 1).astype(bool), y=vy[..., :3].copy(), radiance=vl[..., :3].astype(np.float64),
+                    strategy=(code >> 1).astype(np.uint8))
+    out = RenderResult(image=rp.image.cpu().numpy(), vpl=vpl, gbuffer=gbuf,
+                       mean_path_length=1.0 + float(cnt[0]) / max(h * w * spp, 1), nonfinite_count=int(cnt[1]))
+    if want_moments:
+        lm = rp.lum.cpu().numpy()
+        n = float(spp)
+        out.lum_mean = lm[..., 0] / n
+        out.lum_var = np.maximum(lm[..., 1] / n - out.lum_mean ** 2, 0.0) * (n / max(n - 1.0, 1.0))
+    return out

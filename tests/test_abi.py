@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_status(lib):
-    assert lib.pgg_abi_version() == 1
+    assert lib.pgg_abi_version() == 2
     assert lib.pgg_status_string(0) == b"ok"
     assert lib.pgg_status_string(1) == b"invalid argument"
 
@@ -49,6 +49,8 @@ def test_argument_errors_without_device(lib):
     # argument validation happens before any launch
     assert lib.pgg_lobe(-1, None, None, None, None, None, None, None) == 1
     assert lib.pgg_guiding_pass(None, None, None, None, None, None, None, None, None, None) == 1
+    assert lib.pgg_gbuffer_pass(None, None, None, 4, 4, 0, 4, None, None, None, None, None, None, None) == 1
+    assert lib.pgg_render_pass(None, None, None, None, None, None, None) == 1
 
 
 def test_struct_layout_matches_header():
@@ -59,3 +61,8 @@ def test_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.GBuffer) == 5 * 8 + 8
     assert ctypes.sizeof(_lib.GammaIn) == 24
     assert ctypes.sizeof(_lib.Vpl) == 24
+    # render pass structs
+    assert ctypes.sizeof(_lib.Scene) == 8 + 16 + 24
+    assert ctypes.sizeof(_lib.Camera) == 13 * 8
+    assert ctypes.sizeof(_lib.RenderConfig) == 8 * 4 + 8
+    assert ctypes.sizeof(_lib.RenderOut) == 5 * 8

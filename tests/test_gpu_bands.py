@@ -38,8 +38,10 @@ def _local_exchange(bands):
                         t[lo - ext.lo:hi - ext.lo].copy_(src[lo - next_.lo:hi - next_.lo])
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_bands_match_whole_frame(cuda_dev, world):
+@pytest.mark.parametrize("world,split", [(2, False), (3, False), (5, False), (2, True), (3, True)])
+def test_bands_match_whole_frame(cuda_dev, world, split):
+    """split=True: interior rows and edge rows in separate launches, as in the
+    overlapped exchange path."""
     from paper_2112_09728_b200 import synth
     from paper_2112_09728_b200.bands import BandedGuiding
     from paper_2112_09728_b200.layout import GBufferPlanes, PassConfig, VplPlanes
@@ -55,7 +57,7 @@ def test_bands_match_whole_frame(cuda_dev, world):
             _fill(b, g, v)
         _local_exchange(bands)
         for b in bands:
-            b.step(f, exchange=False)
+            b.step(f, exchange=False, split=split)
         torch.cuda.synchronize()
         g0 = torch.cat([b.gamma_own[0] for b in bands])
         g1 = torch.cat([b.gamma_own[1] for b in bands])
