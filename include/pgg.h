@@ -29,6 +29,7 @@
  *   pgg_render_pass ...... ptrace.render_frame / _render_chunk / _trace_lanes
  *                          ptrace.py:223-355, 382-586 (scene.intersect,
  *                          occluded, sample_emitter, brdf_* scene.py:158-414)
+ *   pgg_image_error ...... metrics.mse / rel_mse         metrics.py:24-38
  *
  * Conventions: every pointer is a DEVICE pointer owned by the caller unless
  * stated otherwise; calls are asynchronous on `stream` (a cudaStream_t, NULL =
@@ -247,6 +248,14 @@ typedef struct pgg_render_out {
  * nee_draws = nee && n_emit ? 3 : 0). */
 int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const pgg_gbuffer* gb, const int32_t* mat,
                     const pgg_samples* depth0, const pgg_render_out* out, void* stream);
+
+/* Image error (metrics.mse / metrics.rel_mse, metrics.py:24-38) of n
+ * float32 elements: mean of (a - ref)^2, or of (a - ref)^2 / (ref^2 + 0.01)
+ * when relative != 0, accumulated in float64 with a fixed reduction order
+ * (deterministic).  scratch: 592 doubles of device memory; out: one double
+ * (device). */
+int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relative, double* scratch, double* out,
+                    void* stream);
 
 const char* pgg_status_string(int status);
 const char* pgg_last_cuda_error(void);

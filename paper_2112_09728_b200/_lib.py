@@ -94,6 +94,7 @@ _SIGS = {
                          c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_render_pass": [ctypes.POINTER(RenderConfig), ctypes.POINTER(Scene), ctypes.POINTER(GBuffer), c_p,
                         ctypes.POINTER(Samples), ctypes.POINTER(RenderOut), c_p],
+    "pgg_image_error": [c_i64, c_p, c_p, c_i32, c_p, c_p, c_p],
 }
 
 EXPORTS = tuple(_SIGS) + ("pgg_frame_key", "pgg_status_string", "pgg_last_cuda_error", "pgg_abi_version")

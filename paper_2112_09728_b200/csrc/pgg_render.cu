@@ -543,6 +543,62 @@ __global__ void __launch_bounds__(128) k_render(const RenderArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Image error metrics (pg/metrics.py:24-47): float64 per-element terms,
+// deterministic two-level reduction (fixed grid, fixed tree), no atomics.
+
+constexpr int ERR_BLOCKS = 592;  // 4 x 148 SMs
+constexpr int ERR_THREADS = 256;
+
+__device__ __forceinline__ double err_term(float a, float r, int rel) {
+  const double d = (double)a - (double)r;
+  const double e = d * d;
+  if (!rel) return e;
+  const double rr = (double)r;
+  return e / (rr * rr + 0.01);
+}
+
+__device__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = 0.0;
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? sh[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(ERR_THREADS) k_err_partial(int64_t n, const float* __restrict__ a,
+                                                            const float* __restrict__ r, int rel, double* part) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 4 float4 per step when aligned: the pass is HBM-bound (8 B read per element)
+  const int64_t n4 = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(r)) & 15) ? 0 : n / 4;
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* r4 = reinterpret_cast<const float4*>(r);
+  for (; i < n4; i += stride) {
+    const float4 x = a4[i], y = r4[i];
+    acc += ((err_term(x.x, y.x, rel) + err_term(x.y, y.y, rel)) + err_term(x.z, y.z, rel)) + err_term(x.w, y.w, rel);
+  }
+  for (int64_t j = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+    acc += err_term(a[j], r[j], rel);
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(ERR_THREADS) k_err_final(int nb, const double* part, int64_t n, double* out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += part[i];
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) *out = s / (double)n;
+}
+
 int table_doubles(const pgg_scene* s) {
   return s->n_mat * MAT_STRIDE + s->n_sph * SPH_STRIDE + s->n_quad * QUAD_STRIDE + s->n_emit;
 }
@@ -605,6 +661,15 @@ int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const 
   A.out = *out;
   const dim3 blk(32, 4), grd((cfg->width + 31) / 32, (cfg->rows + 3) / 4);
   k_render<<<grd, blk, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  return pgg_rt::check_launch();
+}
+
+int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relative, double* scratch, double* out,
+                    void* stream) {
+  if (n <= 0 || !a || !ref || !scratch || !out) return PGG_ERR_ARGUMENT;
+  const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  k_err_partial<<<ERR_BLOCKS, ERR_THREADS, 0, st>>>(n, a, ref, relative ? 1 : 0, scratch);
+  k_err_final<<<1, ERR_THREADS, 0, st>>>(ERR_BLOCKS, scratch, n, out);
   return pgg_rt::check_launch();
 }
 

@@ -1,0 +1,97 @@
+"""GPU: metrics kernels vs NumPy float64, the device-resident RenderSession
+vs the reference-shaped drop-in functions (same kernels, bitwise), and the
+CLI subcommands end to end."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_metrics_match_numpy(cuda_dev):
+    from paper_2112_09728_b200 import metrics
+    r = np.random.default_rng(0)
+    for shape in [(37, 53, 3), (256, 256, 3), (1, 1, 3)]:
+        a = r.exponential(1.0, shape).astype(np.float32)
+        b = (a * r.uniform(0.5, 1.5, shape)).astype(np.float32)
+        ref_mse = float(np.mean((a.astype(np.float64) - b) ** 2))
+        ref_rel = float(np.mean((a.astype(np.float64) - b) ** 2 / (b.astype(np.float64) ** 2 + 0.01)))
+        assert metrics.mse(a, b) == pytest.approx(ref_mse, rel=1e-12)
+        assert metrics.rel_mse(a, b) == pytest.approx(ref_rel, rel=1e-12)
+        assert metrics.mse(torch.from_numpy(a).to(cuda_dev), b) == pytest.approx(ref_mse, rel=1e-12)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        metrics.mse(np.zeros((2, 2, 3), np.float32), np.zeros((2, 3, 3), np.float32))
+    fr = [r.random((8, 8, 3)).astype(np.float32) for _ in range(4)]
+    rows = metrics.flicker_series(fr)
+    assert [x.frame for x in rows] == [0, 1, 2] and rows[1].metric == "temporal_mse"
+    assert rows[2].value == pytest.approx(float(np.mean((fr[2].astype(np.float64) - fr[3]) ** 2)), rel=1e-12)
+    with pytest.raises(ValueError):
+        metrics.flicker_series(fr[:1])
+
+
+def test_session_matches_dropin_functions(cuda_dev):
+    """RenderSession (device-resident frame loop) == the reference-shaped
+    functions chained as pg/cli.py:114-142 does, bit for bit."""
+    from paper_2112_09728_b200 import cli, ptrace
+    from paper_2112_09728_b200 import guide_buffers as gb
+    from paper_2112_09728_b200 import scene as S
+    doc = S.BUILTIN_SCENES["glossy-box"]()
+    k0 = dict(doc["camera"][0])
+    doc["camera"] = [k0, dict(k0, frame=6, origin=[1.1, 0.97, 0.2])]
+    scene = S.scene_from_dict(doc)
+    cfg = cli.RunConfig(width=48, height=36, spp=2, mode="pg", seed=4)
+    sess = cli.RenderSession(scene, cfg)
+    gamma = gb.GuidingBuffer.create(cfg.width, cfg.height)
+    gprev = cam_prev = None
+    pcfg = cfg.path_config(True)
+    for f in range(4):
+        res = sess.run_frame(f)
+        cam = S.camera_at(scene, f)
+        g = ptrace.gbuffer_pass(scene, f, (cfg.width, cfg.height))
+        if gprev is not None:
+            g.motion, g.has_history = ptrace.motion_vectors(cam_prev, cam, g)
+            gamma = gb.reproject(gamma, gprev, g, cfg.policy())
+        r = ptrace.render_frame(scene, f, gamma.stats_for_render(), pcfg, cfg.seed, gbuf=g)
+        gamma = gb.training_pass(gamma, r.vpl, g, k_max=cfg.kmax, seed=cfg.seed, frame_index=f,
+                                 neighbor_radius=cfg.neighbor_radius)
+        gprev, cam_prev = g, cam
+        np.testing.assert_array_equal(res.image.cpu().numpy(), r.image)
+        np.testing.assert_array_equal(sess.gamma.to_aos().cpu().numpy(), gamma.stats)
+        assert res.mean_path_length == pytest.approx(r.mean_path_length)
+
+
+def test_cli_commands(cuda_dev, tmp_path):
+    from paper_2112_09728_b200 import cli, metrics
+    out = str(tmp_path / "r")
+    assert cli.main(["render", "--scene", "cornell-occluder", "--width", "40", "--height", "32", "--frames", "3",
+                     "--mode", "pg", "--spp", "2", "--out", out, "--checkpoint-out", str(tmp_path / "g.pgg")]) == 0
+    for f in range(3):
+        assert os.path.exists(os.path.join(out, f"frame_{f:04d}.pfm"))
+        assert os.path.exists(os.path.join(out, f"frame_{f:04d}.ppm"))
+    lines = open(os.path.join(out, "timing.csv")).read().splitlines()
+    assert lines[0] == "frame,pass,wall_ms,mean_path_length" and len(lines) == 4
+    # resume from the checkpoint
+    assert cli.main(["render", "--width", "40", "--height", "32", "--mode", "pg", "--out", out,
+                     "--checkpoint-in", str(tmp_path / "g.pgg")]) == 0
+    assert cli.main(["render", "--width", "41", "--height", "32", "--mode", "pg", "--out", out,
+                     "--checkpoint-in", str(tmp_path / "g.pgg")]) == 1  # size mismatch
+    ref = str(tmp_path / "ref")
+    assert cli.main(["reference", "--width", "40", "--height", "32", "--spp", "16", "--out", ref]) == 0
+    assert cli.main(["compare", os.path.join(out, "frame_0000.pfm"), os.path.join(out, "frame_0001.pfm"),
+                     os.path.join(ref, "reference.pfm"), "--out", str(tmp_path / "c")]) == 0
+    rows = open(tmp_path / "c" / "compare.csv").read().splitlines()
+    assert rows[0] == "metric,image_a,image_b,ratio_b_over_a" and rows[1].startswith("mse,")
+    assert cli.main(["flicker", "--width", "24", "--height", "16", "--frames", "3", "--warmup", "2", "--mode", "pg",
+                     "--out", str(tmp_path / "fl")]) == 0
+    assert len(open(tmp_path / "fl" / "flicker.csv").read().splitlines()) == 3
+    assert cli.main(["ab", "--width", "24", "--height", "16", "--warmup", "3", "--pairs", "2", "--ref-spp", "32",
+                     "--out", str(tmp_path / "ab")]) == 0
+    ab = dict(line.split(",") for line in open(tmp_path / "ab" / "ab_summary.csv").read().splitlines()[1:])
+    assert float(ab["pg_mean_relmse"]) > 0 and float(ab["pt_mean_relmse"]) > 0
+    assert cli.main(["render", "--scene", "no-such-scene", "--out", out]) == 2
+    assert cli.main(["render", "--frames", "0", "--out", out]) == 2
+    img = metrics.read_pfm(os.path.join(out, "frame_0000.pfm"))
+    assert img.shape == (32, 40, 3) and np.isfinite(img).all()
