@@ -322,27 +322,56 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
 
 // candidate offset (rint of r cos, r sin) with float64 re-evaluation near
 // the half-integer rounding boundary (guide_buffers.py:146-149)
-PGG_COLD void disk_offset_d(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
+struct Off2 {
+  int x, y;
+};
+
+PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
   const double rd = radius * sqrt(u01d(ua));
   const double ang = 2.0 * K<double>::pi * u01d(ub);
-  dx = (int)rint(rd * cos(ang));
-  dy = (int)rint(rd * sin(ang));
+  return {(int)rint(rd * cos(ang)), (int)rint(rd * sin(ang))};
 }
 
+#ifndef PGG_EM_FAST
+#define PGG_EM_FAST 1
+#endif
+
+// float32 candidate offset; values within `band` of a rounding boundary are
+// re-evaluated in float64.  The band (4e-6 (R + 1)) bounds the float32
+// error of r cos / r sin: on the device sin/cos come from MUFU.SIN/COS on
+// [-pi, pi) (abs error < 2^-20.5, x R) and rint from the 1.5 * 2^23 add.
 PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
   const float r = (float)radius * f_sqrt(u01f(ua));
+  const float band = 4e-6f * ((float)radius + 1.0f);
+#if defined(__CUDA_ARCH__) && PGG_EM_FAST
+  const float th = (float)(int32_t)ub * 1.4629180792671596e-09f;  // 2 pi u - (u >= 1/2 ? 2 pi : 0)
+  const float fx = r * __cosf(th), fy = r * __sinf(th);
+  const float kM = 12582912.0f;  // 1.5 * 2^23: x + kM rounds x to the nearest integer (even on ties)
+  const float tx = fx + kM, ty = fy + kM;
+  const float rx = fx - (tx - kM), ry = fy - (ty - kM);
+  if (0.5f - fabsf(rx) < band || 0.5f - fabsf(ry) < band) {
+    const Off2 o = disk_offset_d(ua, ub, radius);
+    dx = o.x;
+    dy = o.y;
+    return;
+  }
+  dx = __float_as_int(tx) - 0x4B400000;
+  dy = __float_as_int(ty) - 0x4B400000;
+#else
   float s, c;
   sincos_turn(ub, &s, &c);
   const float fx = r * c, fy = r * s;
-  const float band = 4e-6f * ((float)radius + 1.0f);
   const float ex = fabsf(fx - floorf(fx) - 0.5f);
   const float ey = fabsf(fy - floorf(fy) - 0.5f);
   if (ex < band || ey < band) {
-    disk_offset_d(ua, ub, radius, dx, dy);
+    const Off2 o = disk_offset_d(ua, ub, radius);
+    dx = o.x;
+    dy = o.y;
     return;
   }
   dx = (int)rintf(fx);
   dy = (int)rintf(fy);
+#endif
 }
 
 // Per-pixel EM context: everything a record needs about its receiver.
@@ -443,8 +472,8 @@ PGG_HD uint32_t pcg_out(uint64_t old) {
 }
 
 // validity thresholds dist > 1e-9 and cos > 1e-9 decided in float64
-PGG_COLD bool record_valid_d(const float4& vy, const V3<float>& x, const V3<float>& n) {
-  const V3<double> dd = cvt<double>(v3(vy.x, vy.y, vy.z)) - cvt<double>(x);
+PGG_COLD bool record_valid_d(float yx, float yy, float yz, V3<float> x, V3<float> n) {
+  const V3<double> dd = cvt<double>(v3(yx, yy, yz)) - cvt<double>(x);
   const double distd = sqrt(dot(dd, dd));
   const V3<double> omd = dd * (1.0 / fmax(distd, 1e-12));
   return distd > 1e-9 && dot(omd, cvt<double>(n)) > 1e-9;
@@ -492,7 +521,7 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
   const V3<float> om = d * rinv;
   const V3<float> dl = S.fr.to_local(om);
   if (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f) {
-    if (!record_valid_d(vy, S.x, S.n_raw)) return false;
+    if (!record_valid_d(vy.x, vy.y, vy.z, S.x, S.n_raw)) return false;
   } else if (!(dl.z > 1e-9f)) {
     return false;
   }
@@ -547,7 +576,7 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
   const V3<float> dl = S.fr.to_local(d * rinv);
   if (ok && (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f)) {
-    ok = record_valid_d(vy, S.x, S.n_raw);
+    ok = record_valid_d(vy.x, vy.y, vy.z, S.x, S.n_raw);
   } else {
     ok = ok && dl.z > 1e-9f;
   }
@@ -583,8 +612,7 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   const float r = num * f_rcp(fmaxf(den, 1e-30f));
   const float wv = ok ? w : 0.0f;
   const float wr = ok ? w * r : 0.0f;
-  qx = ok ? qx : 0.0f;  // masked records may carry NaN from unused inputs
-  qy = ok ? qy : 0.0f;
+  // qx, qy are finite even for masked records (dir_to_sq_f clamps, NaN -> 0)
   acc[0] += wv;
   acc[1] += wr;
   acc[2] = fmaf(wr, qx, acc[2]);
