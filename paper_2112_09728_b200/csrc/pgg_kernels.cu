@@ -47,11 +47,17 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 //            host build's em_combine)
 //   stage 3  lane = pixel: float64 M-step, Gamma' store
 
-constexpr int TILE_W = 32, TILE_H = 8, THREADS = TILE_W * TILE_H;
+#ifndef PGG_TILE_H
+#define PGG_TILE_H 8
+#endif
+constexpr int TILE_W = 32, TILE_H = PGG_TILE_H, THREADS = TILE_W * TILE_H;
 constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this radius
 
+#ifndef PGG_STASH
+#define PGG_STASH 1
+#endif
 #ifndef PGG_MIN_BLOCKS
-#define PGG_MIN_BLOCKS 2
+#define PGG_MIN_BLOCKS 3  // 80 registers, 24 warps/SM: 0.566 vs 0.595 ms at 2 blocks (a few loop-invariant reloads from L1)
 #endif
 
 // shared-memory carve-up of one block
@@ -62,7 +68,8 @@ struct SmemLayout {
     tile_bytes = tile ? (size_t)cols * rows * 16 : 0;
     off_l = (tile_bytes + 127) & ~(size_t)127;
     off_em = off_l + ((tile_bytes + 127) & ~(size_t)127);
-    const size_t em_bytes = EM_LANES > 1 ? (size_t)TILE_H * EM_WORDS * TILE_W * 4 : 0;
+    // EM_LANES == 1: the lane's Gamma (2 float4) parked during the EM loop
+    const size_t em_bytes = EM_LANES > 1 ? (size_t)TILE_H * EM_WORDS * TILE_W * 4 : (size_t)THREADS * 32;
     const size_t sum_bytes = EM_LANES > 1 ? (size_t)TILE_H * 7 * TILE_W * 4 : 0;
     off_sum = off_em + em_bytes;
     off_bar = off_sum + sum_bytes;
@@ -154,6 +161,12 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
     if (!active) return;
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const int y = A.cfg.row0 + yl;
+#if PGG_STASH
+    // park Gamma in shared memory: 8 registers fewer live across the EM loop
+    float4* stash = reinterpret_cast<float4*>(s_em);
+    stash[threadIdx.x] = g0;
+    stash[THREADS + threadIdx.x] = g1;
+#endif
     if (train) {
       if (kTile) {
         const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
@@ -164,6 +177,10 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
       }
     }
     const int64_t own = (int64_t)yl * A.cfg.width + x;
+#if PGG_STASH
+    g0 = stash[threadIdx.x];
+    g1 = stash[THREADS + threadIdx.x];
+#endif
     float4 o0 = g0, o1 = g1;
     if (train) m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
     st4(A.gout.g0, own, o0);

@@ -382,7 +382,7 @@ struct EmSetup {
   Frame<float> fr;   // orthonormal frame about n/|n|
   V3<float> n_raw;   // stored normal (float64 validity re-check)
   V3<float> wol;     // view in the local frame
-  float alb_r, alb_g, alb_b;
+  float alb_r, alb_g, alb_b;  // luminance-weighted albedo (0.2126 r, 0.7152 g, 0.0722 b)
   float a2, kappa, g1o;  // g1o = G1(cos_o) / (4 cos_o)
   float mx, my, il11, l21, il22, gnorm, pi;  // il11, il22 x c and l21 / c, c = sqrt(log2(e) / 2)
   int flags;         // bit0 train this pixel, bit1 glossy, bit2 cos_o > 0
@@ -536,7 +536,7 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
     if (!(S.flags & 2)) {
       // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
       bp = cr * K<float>::inv_pi;
-      o.w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
+      o.w = (lv.x * S.alb_r + lv.y * S.alb_g + lv.z * S.alb_b) * bp;
     } else {
       // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
       const V3<float> hr = dl + S.wol;
@@ -547,11 +547,12 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
       const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
       const float t2 = t * t;
       const float f5 = t2 * t2 * t;
-      const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
-      const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
-      const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
+      // luma_c F_c = la_c + (luma_c - la_c) f5 (Schlick, F0 = albedo)
+      const float kr = fmaf(0.2126f - S.alb_r, f5, S.alb_r);
+      const float kg = fmaf(0.7152f - S.alb_g, f5, S.alb_g);
+      const float kb = fmaf(0.0722f - S.alb_b, f5, S.alb_b);
       // f cos = F D G1(wi) G1(wo) / (4 cos_i cos_o) * cos_i
-      o.w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+      o.w = (lv.x * kr + lv.y * kg + lv.z * kb) * spec;
     }
     if (!kAll && !(isfinite(o.w) && o.w >= 0.0f)) return true;  // dropped by the M-step
   }
@@ -569,14 +570,15 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
 // branch-light: the candidate's validity `ok` masks the sums instead of
 // branching (a warp with mixed validity pays the full record either way),
 // so the record and the next slot's draws form one schedulable block.
-template <class VS, class IDX>
-PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX idx, bool ok, float* acc) {
+template <class VS, class IDX, class NRM>
+PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX idx, bool ok, float* acc,
+                          const NRM& n_raw) {
   const V3<float> d = v3(vy.x, vy.y, vy.z) - S.x;
   const float dist2 = dot(d, d);
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
   const V3<float> dl = S.fr.to_local(d * rinv);
   if (ok && (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f)) {
-    ok = record_valid_d(vy.x, vy.y, vy.z, S.x, S.n_raw);
+    ok = record_valid_d(vy.x, vy.y, vy.z, S.x, n_raw());  // stored normal, reloaded: not live in the loop
   } else {
     ok = ok && dl.z > 1e-9f;
   }
@@ -584,7 +586,7 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   const float4 lv = V.L_at(idx);
   // Lambert (scene.py:269, 296)
   float bp = cr * K<float>::inv_pi;
-  float w = (lv.x * (0.2126f * S.alb_r) + lv.y * (0.7152f * S.alb_g) + lv.z * (0.0722f * S.alb_b)) * bp;
+  float w = (lv.x * S.alb_r + lv.y * S.alb_g + lv.z * S.alb_b) * bp;
   if (S.flags & 2) {
     // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
     const V3<float> hr = dl + S.wol;
@@ -595,10 +597,10 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
     const float t = fminf(fmaxf(1.0f - hi, 0.0f), 1.0f);
     const float t2 = t * t;
     const float f5 = t2 * t2 * t;
-    const float fr_ = S.alb_r + (1.0f - S.alb_r) * f5;
-    const float fg_ = S.alb_g + (1.0f - S.alb_g) * f5;
-    const float fb_ = S.alb_b + (1.0f - S.alb_b) * f5;
-    w = ((lv.x * fr_) * 0.2126f + (lv.y * fg_) * 0.7152f + (lv.z * fb_) * 0.0722f) * spec;
+    const float kr = fmaf(0.2126f - S.alb_r, f5, S.alb_r);
+    const float kg = fmaf(0.7152f - S.alb_g, f5, S.alb_g);
+    const float kb = fmaf(0.0722f - S.alb_b, f5, S.alb_b);
+    w = (lv.x * kr + lv.y * kg + lv.z * kb) * spec;
   }
   // non-finite or zero weights are dropped / add nothing (mixture.py:291)
   ok = ok && w > 0.0f && w <= 3.402823466e38f;
@@ -624,7 +626,7 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
 
 template <class VS>
 PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, int cy, float* acc) {
-  em_accumulate(S, vy, V, V.index(cx, cy), true, acc);
+  em_accumulate(S, vy, V, V.index(cx, cy), true, acc, [&]() { return S.n_raw; });
 }
 
 // Partial sums of lane j of a pixel's group: slots j, j + EM_LANES, ... < N.
@@ -645,11 +647,15 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   }
   const auto base = V.index(x, y);
   const int stride = V.stride();
+  const auto n_raw = [&]() {
+    const float4 nd = ld4(A.cur.nd, (int64_t)(y - A.cur.row0) * C.width + x);
+    return v3(nd.x, nd.y, nd.z);
+  };
   int s = j;
   uint64_t sa = 0, sb = 0;
   if (s == 0) {
     const float4 vy = V.y_at(base);
-    em_accumulate(S, vy, V, base, vy.w != 0.0f, acc);
+    em_accumulate(S, vy, V, base, vy.w != 0.0f, acc, n_raw);
     s = EM_LANES;
   }
   if (s >= S.nb) return;
@@ -678,7 +684,7 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     const auto idx = ok ? base + (decltype(base))dy * stride + dx : base;
     const float4 vy = V.y_at(idx);
     ok = ok && vy.w != 0.0f;  // VPL invalid or not BRDF-strategy
-    em_accumulate(S, vy, V, idx, ok, acc);
+    em_accumulate(S, vy, V, idx, ok, acc, n_raw);
   }
 }
 
@@ -726,9 +732,9 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.x = v3(pr.x, pr.y, pr.z);
   S.fr = pf.fr;
   S.wol = pf.wol;
-  S.alb_r = va.w;
-  S.alb_g = am.x;
-  S.alb_b = am.y;
+  S.alb_r = 0.2126f * va.w;
+  S.alb_g = 0.7152f * am.x;
+  S.alb_b = 0.0722f * am.y;
   S.a2 = alpha * alpha;
   S.kappa = kappa_world(pf.om_nn, S.a2);
   S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
@@ -890,9 +896,9 @@ PGG_HD bool em_setup_from_planes(const PassArgs& A, int x, int y, const float4& 
   S.fr = pf.fr;
   S.n_raw = n;
   S.wol = pf.wol;
-  S.alb_r = va.w;
-  S.alb_g = am.x;
-  S.alb_b = am.y;
+  S.alb_r = 0.2126f * va.w;
+  S.alb_g = 0.7152f * am.x;
+  S.alb_b = 0.0722f * am.y;
   S.a2 = alpha * alpha;
   S.kappa = kappa_world(pf.om_nn, S.a2);
   S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
