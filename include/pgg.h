@@ -202,7 +202,7 @@ int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream);
  * Render pass (the producer of the G-buffer and the VPLs). */
 
 /* Scene table (device, float64; built by paper_2112_09728_b200/scene.py
- * Scene.pack): n_mat x 8 (kind, albedo rgb, roughness, emission rgb),
+ * Scene.pack): n_mat x 12 (kind, albedo rgb, roughness, emission rgb, albedo/pi rgb, pad),
  * n_sph x 8 (center xyz, radius, material, pad), n_quad x 16 (corner, edge_u,
  * edge_v, unit normal, area, material, |edge_u|^2, |edge_v|^2), n_emit
  * emitter quad indices.  At most 6144 doubles (staged in shared memory). */

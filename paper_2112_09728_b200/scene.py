@@ -22,7 +22,7 @@ LUMA_WEIGHTS = np.array([0.2126, 0.7152, 0.0722])
 RAY_EPS = 1e-4  # pg/scene.py:24
 
 # packed table layout (doubles per record), shared with pgg_render.cuh
-MAT_STRIDE = 8    # kind, albedo rgb, roughness, emission rgb
+MAT_STRIDE = 12   # kind, albedo rgb, roughness, emission rgb, albedo / pi rgb, pad
 SPH_STRIDE = 8    # center xyz, radius, material, pad x3
 QUAD_STRIDE = 16  # corner xyz, eu xyz, ev xyz, normal xyz, area, material, |eu|^2, |ev|^2
 
@@ -94,6 +94,7 @@ class Scene:
         mats[:, 1:4] = self.mat_albedo
         mats[:, 4] = self.mat_rough
         mats[:, 5:8] = self.mat_emission
+        mats[:, 8:11] = self.mat_albedo / np.pi  # the reference's Lambert value (pg/scene.py:268), same rounding
         sph = np.zeros((ns, SPH_STRIDE))
         if ns:
             sph[:, 0:3] = self.sph_center
