@@ -69,12 +69,12 @@ PGG_HD uint8_t ldu8(const uint8_t* p, int64_t i) {
 #endif
 }
 
-PGG_HD void count_miss(int32_t* c) {
+PGG_HD void count_miss(int32_t* c, int n = 1) {
   if (!c) return;
 #ifdef __CUDA_ARCH__
-  atomicAdd(c, 1);
+  atomicAdd(c, n);
 #else
-  *c += 1;
+  *c += n;
 #endif
 }
 
@@ -669,6 +669,7 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
 #elif PGG_EM_UNROLL == 3
 #pragma unroll 3
 #endif
+  int misses = 0;  // in-frame candidates outside the supplied VPL rows (halo misses)
   for (; s < S.nb; s += EM_LANES) {
     const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
     sa = sa * JL_MUL + JL_ADD;
@@ -676,16 +677,16 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     int dx, dy;
     disk_offset(ua, ub, C.radius, dx, dy);
     const int cx = x + dx, cy = y + dy;
-    bool ok = (unsigned)cx < W && (unsigned)cy < H;
-    if (ok && (unsigned)(cy - vr0) >= vrows) {
-      count_miss(A.halo_misses);
-      ok = false;
-    }
+    const bool in_frame = (unsigned)cx < W && (unsigned)cy < H;
+    const bool in_vpl = (unsigned)(cy - vr0) < vrows;
+    misses += (in_frame && !in_vpl) ? 1 : 0;
+    bool ok = in_frame && in_vpl;
     const auto idx = ok ? base + (decltype(base))dy * stride + dx : base;
     const float4 vy = V.y_at(idx);
     ok = ok && vy.w != 0.0f;  // VPL invalid or not BRDF-strategy
     em_accumulate(S, vy, V, idx, ok, acc, n_raw);
   }
+  if (misses) count_miss(A.halo_misses, misses);
 }
 
 // The butterfly order of the device reduction (xor EM_LANES/2, ..., 1), so
