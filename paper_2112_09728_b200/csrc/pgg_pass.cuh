@@ -749,6 +749,9 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.pi = L.pi;
   S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
   S.nb = neighbor_budget(k, kmax);
+#ifdef PGG_PROF_NO_EM
+  S.nb = 0;  // measurement-only build: stage 1 alone
+#endif
   S.s0 = s0;
 }
 
@@ -771,7 +774,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   const float4 pr = ld4(A.cur.pr, ci);
   const float4 am = ld4(A.cur.am, ci);
   const float4 va = ld4(A.cur.va, ci);
+#ifdef PGG_PROF_NO_REPROJ
+  if (false) {  // measurement-only build
+#else
   if (A.has_prev) {
+#endif
     reproject_px(A, x, y, fl, nd, pr, am, g0, g1);
   } else {
     const int64_t gi = (int64_t)(y - A.gin.row0) * W + x;
@@ -801,7 +808,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   const bool glossy = (fl & 4) != 0;
   const PixelFrame pf = make_pixel_frame(n, wo);
   const uint64_t pix = (uint64_t)y * (uint64_t)W + (uint64_t)x;
+#ifdef PGG_PROF_NO_SMP
+  if (false) {  // measurement-only build
+#else
   if (A.has_smp) {
+#endif
     const bool guided = (!glossy || (double)rough >= C.rough_min_guide) && g1.w >= 1.0f;
     CholD cd;
     cd.mx = g0.x;
