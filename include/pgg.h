@@ -239,6 +239,9 @@ typedef struct pgg_render_out {
   float* vpl_L;
   double* lum_moments;            /* rows x W x 2 (sum, sum of squares of luminance) or NULL */
   unsigned long long* counters;   /* [scatter segments, non-finite samples] accumulated, or NULL */
+  uint64_t* states;               /* NULL: lane streams from cfg.key (ptrace.py:474-475); else the
+                                     caller's PCG32 state per lane (band-local lane index), advanced in
+                                     place (ptrace.trace_pixel, ptrace.py:358-376) */
 } pgg_render_out;
 
 /* Trace spp lanes per pixel from the G-buffer (gb + mat planes holding the
@@ -248,6 +251,30 @@ typedef struct pgg_render_out {
  * nee_draws = nee && n_emit ? 3 : 0). */
 int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const pgg_gbuffer* gb, const int32_t* mat,
                     const pgg_samples* depth0, const pgg_render_out* out, void* stream);
+
+/* Scene routines of pg/scene.py as batch lane operations (float64, n lanes,
+ * xyz triples interleaved):
+ *   pgg_intersect ....... scene.intersect / occluded (scene.py:158-241):
+ *                         any_hit != 0 writes only `hit` (occluded)
+ *   pgg_sample_emitter .. scene.sample_emitter (scene.py:386-414), three
+ *                         draws per lane from `states` (in/out)
+ *   pgg_brdf ............ op 0 brdf_eval -> f (rgb), 1 brdf_pdf -> pdf,
+ *                         2 brdf_sample -> wi, pdf, valid (two draws)
+ *                         (scene.py:258-380)
+ *   pgg_primary_rays .... scene.primary_ray_dirs (scene.py:125-135)
+ *   pgg_project ......... scene.project_to_pixels (scene.py:138-151) */
+int pgg_intersect(const pgg_scene* scene, int64_t n, const double* origins, const double* dirs, const double* t_min,
+                  const double* t_max, int32_t any_hit, uint8_t* hit, double* t, double* pos, double* normal,
+                  int32_t* mat, uint8_t* front, void* stream);
+int pgg_sample_emitter(const pgg_scene* scene, int64_t n, const double* points, uint64_t* states, double* dir,
+                       double* dist, double* emitted, double* pdf, void* stream);
+int pgg_brdf(int32_t op, int64_t n, const int32_t* kind, const double* albedo, const double* rough, double* wi,
+             const double* wo, const double* normal, uint64_t* states, double* f, double* pdf, uint8_t* valid,
+             void* stream);
+int pgg_primary_rays(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* px,
+                     const double* py, double* dirs, void* stream);
+int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* points, double* px,
+                double* py, uint8_t* in_front, void* stream);
 
 /* Image error (metrics.mse / metrics.rel_mse, metrics.py:24-38) of n
  * float32 elements: mean of (a - ref)^2, or of (a - ref)^2 / (ref^2 + 0.01)

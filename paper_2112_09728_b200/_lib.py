@@ -70,7 +70,8 @@ class RenderConfig(ctypes.Structure):
 
 
 class RenderOut(ctypes.Structure):
-    _fields_ = [("image", c_p), ("vpl_y", c_p), ("vpl_L", c_p), ("lum_moments", c_p), ("counters", c_p)]
+    _fields_ = [("image", c_p), ("vpl_y", c_p), ("vpl_L", c_p), ("lum_moments", c_p), ("counters", c_p),
+                ("states", c_p)]
 
 
 _SIGS = {
@@ -95,6 +96,11 @@ _SIGS = {
     "pgg_render_pass": [ctypes.POINTER(RenderConfig), ctypes.POINTER(Scene), ctypes.POINTER(GBuffer), c_p,
                         ctypes.POINTER(Samples), ctypes.POINTER(RenderOut), c_p],
     "pgg_image_error": [c_i64, c_p, c_p, c_i32, c_p, c_p, c_p],
+    "pgg_intersect": [ctypes.POINTER(Scene), c_i64, c_p, c_p, c_p, c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "pgg_sample_emitter": [ctypes.POINTER(Scene), c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "pgg_brdf": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "pgg_primary_rays": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p],
+    "pgg_project": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p],
 }
 
 EXPORTS = tuple(_SIGS) + ("pgg_frame_key", "pgg_status_string", "pgg_last_cuda_error", "pgg_abi_version")

@@ -437,7 +437,7 @@ __global__ void k_sample_lanes(int64_t n, int world, const float4* __restrict__ 
   const LaneOut o = sample_lane(pf, glossy[i] != 0, rough[i], gd, L, cd, st);
   states[i] = st;
   dir[i] = f4(o.wi.x, o.wi.y, o.wi.z, o.pdf);
-  tag[i] = (uint8_t)(o.gauss | (o.valid << 1));
+  tag[i] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
 }
 
 // ---------------------------------------------------------------------------

@@ -411,7 +411,7 @@ struct LaneResult {
 };
 
 __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool valid0, bool front0, D3 pos, D3 nrm,
-                                 int mat, D3 wo, uint64_t st, int64_t lane_own) {
+                                 int mat, D3 wo, uint64_t& st, int64_t lane_own) {
   const pgg_render_config& C = A.cfg;
   LaneResult R;
   R.L = d3(0, 0, 0);
@@ -512,9 +512,11 @@ __device__ void render_pixel(const RenderArgs& A, const SceneS& S, int x, int yl
   double lsum = 0.0, lsq = 0.0;
   LaneResult R;
   for (int s = 0; s < C.spp; ++s) {
-    const uint64_t st = pcg_lane(C.key, pix * (uint64_t)C.spp + (uint64_t)s);
+    const int64_t lane = own * C.spp + s;
+    uint64_t st = A.out.states ? A.out.states[lane] : pcg_lane(C.key, pix * (uint64_t)C.spp + (uint64_t)s);
     R = trace_lane(A, S, valid, front, d3(pr.x, pr.y, pr.z), d3(nd.x, nd.y, nd.z), m, d3(va.x, va.y, va.z), st,
                    own * C.spp + s);
+    if (A.out.states) A.out.states[lane] = st;
     segs += R.segs;
     if (!finite3(R.L)) {
       ++bad;
@@ -623,6 +625,111 @@ __global__ void __launch_bounds__(ERR_THREADS) k_err_final(int nb, const double*
   if (threadIdx.x == 0) *out = s / (double)n;
 }
 
+
+// ---------------------------------------------------------------------------
+// Lane kernels: the scene routines of pg/scene.py as batch operations
+// (intersect / occluded, sample_emitter, brdf_eval / brdf_pdf /
+// brdf_sample, primary_ray_dirs, project_to_pixels), float64 in / out.
+
+__device__ __forceinline__ D3 ldd3(const double* p, int64_t i) { return d3(p[3 * i], p[3 * i + 1], p[3 * i + 2]); }
+__device__ __forceinline__ void std3(double* p, int64_t i, D3 v) {
+  p[3 * i] = v.x;
+  p[3 * i + 1] = v.y;
+  p[3 * i + 2] = v.z;
+}
+
+__global__ void __launch_bounds__(128) k_lane_intersect(const pgg_scene sc, int64_t n, const double* o, const double* d,
+                                                        const double* t_min, const double* t_max, int any_hit,
+                                                        uint8_t* hit, double* t, double* pos, double* nrm,
+                                                        int32_t* mat, uint8_t* front) {
+  extern __shared__ double smem[];
+  const SceneS S = stage_scene(sc, smem);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const D3 oi = ldd3(o, i), di = ldd3(d, i);
+  if (any_hit) {
+    hit[i] = cast<true>(S, oi, di, t_min[i], t_max[i]).hit ? 1 : 0;
+    return;
+  }
+  const Hit h = cast<false>(S, oi, di, t_min[i], t_max[i]);
+  hit[i] = h.hit ? 1 : 0;
+  t[i] = h.hit ? h.t : INFINITY;
+  // the reference's pos = o + best_t d is non-finite on a miss (best_t = inf)
+  std3(pos, i, h.hit ? h.pos : oi + di * INFINITY);
+  std3(nrm, i, h.hit ? h.nrm : d3(0, 0, 0));
+  mat[i] = h.hit ? h.mat : -1;
+  front[i] = h.front ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(128) k_lane_emitter(const pgg_scene sc, int64_t n, const double* pts,
+                                                      uint64_t* states, double* dir, double* dist, double* le,
+                                                      double* pdf) {
+  extern __shared__ double smem[];
+  const SceneS S = stage_scene(sc, smem);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || S.ne == 0) return;
+  uint64_t st = states[i];
+  D3 w, e;
+  double ds, p;
+  sample_emitter(S, ldd3(pts, i), st, w, ds, e, p);
+  states[i] = st;
+  std3(dir, i, w);
+  dist[i] = ds;
+  std3(le, i, e);
+  pdf[i] = p;
+}
+
+// op 0: eval (f rgb), 1: pdf, 2: sample (wi, pdf, valid; two draws per lane)
+__global__ void __launch_bounds__(128) k_lane_brdf(int op, int64_t n, const int32_t* kind, const double* alb,
+                                                   const double* rough, double* wi, const double* wo, const double* nn,
+                                                   uint64_t* states, double* f, double* pdf, uint8_t* valid) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = kind[i];
+  const D3 woi = ldd3(wo, i), ni = ldd3(nn, i);
+  if (op == 0) {
+    const D3 a = ldd3(alb, i);
+    std3(f, i, brdf_eval(k, a, a / PI_D, rough[i], ldd3(wi, i), woi, ni));
+  } else if (op == 1) {
+    pdf[i] = brdf_pdf(k, rough[i], ldd3(wi, i), woi, ni);
+  } else {
+    uint64_t st = states[i];
+    double p;
+    bool ok;
+    const D3 w = brdf_sample(k, rough[i], woi, ni, st, p, ok);
+    states[i] = st;
+    std3(wi, i, w);
+    pdf[i] = p;
+    valid[i] = ok ? 1 : 0;
+  }
+}
+
+// primary_ray_dirs (pg/scene.py:125-135) and project_to_pixels (138-151)
+__global__ void k_lane_rays(pgg_camera cam, int w, int h, int64_t n, const double* px, const double* py, double* dirs) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double aspect = (double)w / (double)h;
+  const double nx = (2.0 * (px[i] + 0.5) / (double)w - 1.0) * cam.tan_half_fov * aspect;
+  const double ny = (1.0 - 2.0 * (py[i] + 0.5) / (double)h) * cam.tan_half_fov;
+  std3(dirs, i, normalize((cam3(cam.forward) + cam3(cam.right) * nx) + cam3(cam.up) * ny));
+}
+
+__global__ void k_lane_project(pgg_camera cam, int w, int h, int64_t n, const double* pts, double* px, double* py,
+                               uint8_t* in_front) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double aspect = (double)w / (double)h;
+  const D3 dd = ldd3(pts, i) - cam3(cam.origin);
+  const double zc = dot(dd, cam3(cam.forward));
+  const bool fr = zc > 1e-9;
+  const double z = fr ? zc : 1.0;
+  const double xc = dot(dd, cam3(cam.right)) / z;
+  const double yc = dot(dd, cam3(cam.up)) / z;
+  px[i] = (xc / (cam.tan_half_fov * aspect) + 1.0) * 0.5 * (double)w - 0.5;
+  py[i] = (1.0 - yc / cam.tan_half_fov) * 0.5 * (double)h - 0.5;
+  in_front[i] = fr ? 1 : 0;
+}
+
 int table_doubles(const pgg_scene* s) {
   return s->n_mat * MAT_STRIDE + s->n_sph * SPH_STRIDE + s->n_quad * QUAD_STRIDE + s->n_emit;
 }
@@ -694,6 +801,59 @@ int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relativ
   const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   k_err_partial<<<ERR_BLOCKS, ERR_THREADS, 0, st>>>(n, a, ref, relative ? 1 : 0, scratch);
   k_err_final<<<1, ERR_THREADS, 0, st>>>(ERR_BLOCKS, scratch, n, out);
+  return pgg_rt::check_launch();
+}
+
+static inline unsigned lane_blocks(int64_t n) { return (unsigned)((n + 127) / 128); }
+
+int pgg_intersect(const pgg_scene* scene, int64_t n, const double* origins, const double* dirs, const double* t_min,
+                  const double* t_max, int32_t any_hit, uint8_t* hit, double* t, double* pos, double* normal,
+                  int32_t* mat, uint8_t* front, void* stream) {
+  if (!scene_ok(scene) || n < 0 || !origins || !dirs || !t_min || !t_max || !hit) return PGG_ERR_ARGUMENT;
+  if (!any_hit && (!t || !pos || !normal || !mat || !front)) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_intersect<<<lane_blocks(n), 128, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(
+      *scene, n, origins, dirs, t_min, t_max, any_hit, hit, t, pos, normal, mat, front);
+  return pgg_rt::check_launch();
+}
+
+int pgg_sample_emitter(const pgg_scene* scene, int64_t n, const double* points, uint64_t* states, double* dir,
+                       double* dist, double* emitted, double* pdf, void* stream) {
+  if (!scene_ok(scene) || scene->n_emit < 1 || n < 0 || !points || !states || !dir || !dist || !emitted || !pdf)
+    return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_emitter<<<lane_blocks(n), 128, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(
+      *scene, n, points, states, dir, dist, emitted, pdf);
+  return pgg_rt::check_launch();
+}
+
+int pgg_brdf(int32_t op, int64_t n, const int32_t* kind, const double* albedo, const double* rough, double* wi,
+             const double* wo, const double* normal, uint64_t* states, double* f, double* pdf, uint8_t* valid,
+             void* stream) {
+  if (op < 0 || op > 2 || n < 0 || !kind || !rough || !wi || !wo || !normal) return PGG_ERR_ARGUMENT;
+  if ((op == 0 && (!albedo || !f)) || (op == 1 && !pdf) || (op == 2 && (!states || !pdf || !valid)))
+    return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_brdf<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(op, n, kind, albedo, rough, wi, wo,
+                                                                                  normal, states, f, pdf, valid);
+  return pgg_rt::check_launch();
+}
+
+int pgg_primary_rays(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* px,
+                     const double* py, double* dirs, void* stream) {
+  if (!cam || width <= 0 || height <= 0 || n < 0 || !px || !py || !dirs) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_rays<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, px, py,
+                                                                                  dirs);
+  return pgg_rt::check_launch();
+}
+
+int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* points, double* px,
+                double* py, uint8_t* in_front, void* stream) {
+  if (!cam || width <= 0 || height <= 0 || n < 0 || !points || !px || !py || !in_front) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_project<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, points,
+                                                                                     px, py, in_front);
   return pgg_rt::check_launch();
 }
 

@@ -276,3 +276,89 @@ def result_from_planes(rp, gbuf, spp, want_moments):
         out.lum_mean = lm[..., 0] / n
         out.lum_var = np.maximum(lm[..., 1] / n - out.lum_mean ** 2, 0.0) * (n / max(n - 1.0, 1.0))
     return out
+
+
+# ---------------------------------------------------------------------------
+# per-pixel API (pg/ptrace.py:79-95, 336-376)
+
+def worker_count():
+    """Host worker threads of the reference's CPU render (PG_THREADS, else
+    the CPU count; pg/ptrace.py:89-95).  The GPU render ignores it."""
+    import os
+    env = os.environ.get("PG_THREADS", "")
+    if env.strip():
+        try:
+            return max(1, int(env))
+        except ValueError:
+            pass
+    return max(1, os.cpu_count() or 1)
+
+
+class PixelHit(NamedTuple):
+    """Single-pixel view of a G-buffer entry (pg/ptrace.py:336-345)."""
+
+    valid: bool
+    pos: np.ndarray
+    normal: np.ndarray
+    mat: int
+    roughness: float
+    front: bool
+    view: np.ndarray
+
+
+_PCG_MUL, _PCG_INC, _M64 = 6364136223846793005, 1442695040888963407, (1 << 64) - 1
+
+
+def trace_pixel(scene, gpx, guiding_entry, cfg, streams):
+    """One path sample for one pixel (pg/ptrace.py:348-376) through the same
+    device kernels as whole frames: the render kernel on a 1x1 G-buffer with
+    the caller's PCG32 state (``streams``, one uint64, advanced in place);
+    ``guiding_entry`` = (stats (8,), GaussianLobe) samples depth 0 from the
+    mixture.  Returns (color (3,), vpl dict); color and VPL come back in the
+    float32 device layout."""
+    from .render import FrameGBuffer, render_planes
+    dev = _conv.device()
+    valid = bool(gpx.valid)
+    mat = int(gpx.mat) if valid else 0
+    kind = int(scene.mat_kind[mat])
+    f64 = lambda v: np.asarray(v, dtype=np.float64).reshape(3)  # noqa: E731
+    pos, nrm, view = f64(gpx.pos), f64(gpx.normal), f64(gpx.view)
+    planes = GBufferPlanes.pack(np.array([[valid]]), pos.reshape(1, 1, 3), nrm.reshape(1, 1, 3), np.zeros((1, 1)),
+                                np.array([[kind]]), np.asarray(scene.mat_albedo[mat]).reshape(1, 1, 3),
+                                np.array([[float(gpx.roughness)]]), view.reshape(1, 1, 3), device=dev)
+    planes.flags |= (1 if (valid and bool(gpx.front)) else 0) << 3
+    planes.height = 1
+    fgb = FrameGBuffer(planes, torch.tensor([[mat if valid else -1]], dtype=torch.int32, device=dev))
+    st0 = int(np.asarray(streams, dtype=np.uint64).reshape(-1)[0]) if not torch.is_tensor(streams) else \
+        int(streams.reshape(-1)[0].item()) & _M64
+    depth0 = None
+    if guiding_entry is not None and valid:
+        stats, lobe = guiding_entry
+        stats = np.asarray(stats, dtype=np.float64).reshape(8)
+        rough_ok = kind == sc.DIFFUSE or float(gpx.roughness) >= cfg.roughness_min_guide
+        if rough_ok and stats[mixture.EPOCH] >= 1.0:
+            s1 = st0
+            for _ in range(3 if (cfg.nee and scene.num_emitters) else 0):
+                s1 = (s1 * _PCG_MUL + _PCG_INC) & _M64
+            lb = mixture.GaussianLobe(np.asarray(lobe.mu, dtype=np.float64).reshape(1, 2),
+                                      np.asarray(lobe.cov, dtype=np.float64).reshape(1, 2, 2),
+                                      np.asarray(lobe.chol, dtype=np.float64).reshape(1, 2, 2),
+                                      np.atleast_1d(np.asarray(lobe.trunc_z, dtype=np.float64)))
+            states1 = torch.tensor([s1 - (1 << 64) if s1 >= (1 << 63) else s1], dtype=torch.int64, device=dev)
+            d, t = mixture.sample_lanes(True, nrm.reshape(1, 3), view.reshape(1, 3), np.array([kind]),
+                                        np.array([scene.mat_rough[mat]]), np.array([1]), np.array([stats[6]]),
+                                        mixture._lobe6(lb), states1)
+            depth0 = SamplePlanes(d.reshape(1, 1, 1, 4).contiguous(), t.reshape(1, 1, 1).contiguous(), 1)
+    states = torch.tensor([st0 - (1 << 64) if st0 >= (1 << 63) else st0], dtype=torch.int64, device=dev)
+    rp = render_planes(_device_scene(scene), fgb, 0, 0, spp=1, max_depth=cfg.max_depth, nee=cfg.nee, depth0=depth0,
+                       states=states)
+    st_out = int(states[0].item()) & _M64
+    if torch.is_tensor(streams):
+        streams.reshape(-1)[0] = st_out - (1 << 64) if st_out >= (1 << 63) else st_out
+    else:
+        np.asarray(streams).reshape(-1)[0] = np.uint64(st_out)
+    color = rp.image[0, 0].to(torch.float64).cpu().numpy()
+    vy = rp.vpl.y[0, 0].to(torch.float64).cpu().numpy()
+    vl = rp.vpl.L[0, 0].to(torch.float64).cpu().numpy()
+    code = int(vl[3])
+    return color, {"valid": bool(code & 1), "y": vy[:3], "radiance": vl[:3], "strategy": code >> 1}

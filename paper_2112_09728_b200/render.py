@@ -96,9 +96,11 @@ class RenderPlanes:
 
 def render_planes(dscene: DeviceScene, fgb: FrameGBuffer, frame, seed, spp=1, max_depth=4, nee=True,
                   depth0: Optional[SamplePlanes] = None, want_moments=False, row0=None, rows=None,
-                  out: Optional[RenderPlanes] = None, stream=None) -> RenderPlanes:
+                  out: Optional[RenderPlanes] = None, stream=None, states: Optional[torch.Tensor] = None) -> RenderPlanes:
     """Trace spp lanes per pixel of rows [row0, row0 + rows) (default: the
-    G-buffer's rows).  depth0: the guiding pass's samples of the same rows."""
+    G-buffer's rows).  depth0: the guiding pass's samples of the same rows.
+    states: caller PCG32 lane states (int64 view, rows*W*spp), advanced in
+    place, instead of the (seed, frame, lane) key chain."""
     g = fgb.planes
     W = g.width
     H = int(g.height if g.height is not None else g.row0 + g.rows)
@@ -118,7 +120,7 @@ def render_planes(dscene: DeviceScene, fgb: FrameGBuffer, frame, seed, spp=1, ma
     c.spp, c.max_depth, c.nee = int(spp), int(max_depth), 1 if nee else 0
     c.key = _lib.frame_key(seed, frame, 0)
     o = _lib.RenderOut(_lib.ptr(out.image), _lib.ptr(out.vpl.y), _lib.ptr(out.vpl.L), _lib.ptr(out.lum),
-                       _lib.ptr(out.counters))
+                       _lib.ptr(out.counters), _lib.ptr(states))
     smp = depth0.as_abi() if depth0 is not None else None
     gabi = g.as_abi()
     _lib.check(_lib.lib().pgg_render_pass(ctypes.byref(c), ctypes.byref(dscene.abi), ctypes.byref(gabi),

@@ -401,3 +401,208 @@ BUILTIN_SCENES = {
     "indirect-corridor": _indirect_corridor,
     "glossy-box": _glossy_box,
 }
+
+
+# ---------------------------------------------------------------------------
+# Scene routines on the GPU (pg/scene.py:125-414), NumPy / torch in and out.
+# Batch entry points of csrc/pgg_render.cu (the same float64 device code the
+# render kernels use); `streams` are advanced in place like the reference's.
+
+def _dev():
+    from . import _conv
+    return _conv.device()
+
+
+def _d64(a, shape=None):
+    import torch
+
+    from . import _conv
+    t = _conv.to_dev(a, torch.float64)
+    return t.reshape(shape) if shape is not None else t
+
+
+def _out(t, like_torch):
+    return t if like_torch else t.cpu().numpy()
+
+
+def _device_scene(scene):
+    from .render import DeviceScene
+    dev = _dev()
+    ds = getattr(scene, "_pgg_device_scene", None)
+    if ds is None or ds.device != dev:
+        ds = DeviceScene(scene, dev)
+        scene._pgg_device_scene = ds
+    return ds
+
+
+def _states_in(streams):
+    import torch
+
+    from . import _conv
+    if torch.is_tensor(streams):
+        return streams.view(torch.int64) if streams.is_cuda else _conv.u64_to_dev(streams)
+    return _conv.u64_to_dev(np.asarray(streams))
+
+
+def _states_back(streams, states):
+    import torch
+    if torch.is_tensor(streams):
+        if not streams.is_cuda:
+            streams.copy_(states.cpu().view(streams.dtype))
+    else:
+        streams[...] = states.cpu().numpy().view(np.uint64).reshape(np.shape(streams))
+
+
+def intersect(scene, origins, dirs, t_min=RAY_EPS, t_max=np.inf):
+    """Nearest hit per ray (pg/scene.py:158-235): dict hit, t, pos, normal, mat, front, is_emitter."""
+    import torch
+
+    from . import _lib
+    like = torch.is_tensor(origins)
+    o = _d64(origins, (-1, 3))
+    d = _d64(dirs, (-1, 3))
+    n = o.shape[0]
+    tmin = torch.broadcast_to(_d64(t_min), (n,)).contiguous()
+    tmax = torch.broadcast_to(_d64(t_max), (n,)).contiguous()
+    ds = _device_scene(scene)
+    hit = torch.empty(n, dtype=torch.uint8, device=o.device)
+    t = torch.empty(n, dtype=torch.float64, device=o.device)
+    pos = torch.empty(n, 3, dtype=torch.float64, device=o.device)
+    nrm = torch.empty(n, 3, dtype=torch.float64, device=o.device)
+    mat = torch.empty(n, dtype=torch.int32, device=o.device)
+    front = torch.empty(n, dtype=torch.uint8, device=o.device)
+    import ctypes
+    _lib.check(_lib.lib().pgg_intersect(ctypes.byref(ds.abi), n, _lib.ptr(o), _lib.ptr(d), _lib.ptr(tmin),
+                                        _lib.ptr(tmax), 0, _lib.ptr(hit), _lib.ptr(t), _lib.ptr(pos), _lib.ptr(nrm),
+                                        _lib.ptr(mat), _lib.ptr(front), _lib.stream_ptr()))
+    h = hit.bool()
+    em = torch.as_tensor(np.any(scene.mat_emission > 0.0, axis=-1), device=o.device)
+    is_em = h & em[mat.clamp(min=0).long()]
+    out = {"hit": h, "t": t, "pos": pos, "normal": nrm, "mat": mat, "front": front.bool(), "is_emitter": is_em}
+    return {k: _out(v, like) for k, v in out.items()}
+
+
+def occluded(scene, origins, dirs, t_max):
+    """True where geometry blocks the segment (RAY_EPS, t_max) (pg/scene.py:238-241)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    like = torch.is_tensor(origins)
+    o = _d64(origins, (-1, 3))
+    d = _d64(dirs, (-1, 3))
+    n = o.shape[0]
+    tmin = torch.full((n,), RAY_EPS, dtype=torch.float64, device=o.device)
+    tmax = torch.broadcast_to(_d64(t_max), (n,)).contiguous()
+    hit = torch.empty(n, dtype=torch.uint8, device=o.device)
+    ds = _device_scene(scene)
+    _lib.check(_lib.lib().pgg_intersect(ctypes.byref(ds.abi), n, _lib.ptr(o), _lib.ptr(d), _lib.ptr(tmin),
+                                        _lib.ptr(tmax), 1, _lib.ptr(hit), None, None, None, None, None,
+                                        _lib.stream_ptr()))
+    return _out(hit.bool(), like)
+
+
+def sample_emitter(scene, points, streams):
+    """NEE toward one uniformly picked quad emitter (pg/scene.py:386-414);
+    three draws per lane, `streams` advanced in place.  Returns (dir, dist, emitted, pdf_sr)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    like = torch.is_tensor(points)
+    p = _d64(points, (-1, 3))
+    n = p.shape[0]
+    st = _states_in(streams).contiguous()
+    dev = p.device
+    w = torch.empty(n, 3, dtype=torch.float64, device=dev)
+    dist = torch.empty(n, dtype=torch.float64, device=dev)
+    le = torch.empty(n, 3, dtype=torch.float64, device=dev)
+    pdf = torch.empty(n, dtype=torch.float64, device=dev)
+    ds = _device_scene(scene)
+    _lib.check(_lib.lib().pgg_sample_emitter(ctypes.byref(ds.abi), n, _lib.ptr(p), _lib.ptr(st), _lib.ptr(w),
+                                             _lib.ptr(dist), _lib.ptr(le), _lib.ptr(pdf), _lib.stream_ptr()))
+    _states_back(streams, st)
+    return tuple(_out(v, like) for v in (w, dist, le, pdf))
+
+
+def _brdf(op, kind, albedo, rough, wi, wo, n, streams=None):
+    import torch
+
+    from . import _conv, _lib
+    like = any(torch.is_tensor(x) for x in (wi, wo, n) if x is not None)
+    wo_t = _d64(wo, (-1, 3))
+    m = wo_t.shape[0]
+    dev = wo_t.device
+    nn = torch.broadcast_to(_d64(n, (-1, 3)), (m, 3)).contiguous()
+    k = torch.broadcast_to(_conv.to_dev(kind, torch.int32).reshape(-1), (m,)).contiguous()
+    r = torch.broadcast_to(_d64(rough).reshape(-1), (m,)).contiguous()
+    alb = torch.broadcast_to(_d64(albedo, (-1, 3)), (m, 3)).contiguous() if albedo is not None else None
+    wi_t = _d64(wi, (-1, 3)).clone() if wi is not None else torch.empty(m, 3, dtype=torch.float64, device=dev)
+    f = torch.empty(m, 3, dtype=torch.float64, device=dev) if op == 0 else None
+    pdf = torch.empty(m, dtype=torch.float64, device=dev) if op >= 1 else None
+    valid = torch.empty(m, dtype=torch.uint8, device=dev) if op == 2 else None
+    st = _states_in(streams).contiguous() if op == 2 else None
+    _lib.check(_lib.lib().pgg_brdf(op, m, _lib.ptr(k), _lib.ptr(alb), _lib.ptr(r), _lib.ptr(wi_t), _lib.ptr(wo_t),
+                                   _lib.ptr(nn), _lib.ptr(st), _lib.ptr(f), _lib.ptr(pdf), _lib.ptr(valid),
+                                   _lib.stream_ptr()))
+    if op == 0:
+        return _out(f, like)
+    if op == 1:
+        return _out(pdf, like)
+    _states_back(streams, st)
+    return _out(wi_t, like), _out(pdf, like), _out(valid.bool(), like)
+
+
+def brdf_eval(kind, albedo, rough, wi, wo, n):
+    """BRDF value (RGB), zero below the surface (pg/scene.py:258-284)."""
+    return _brdf(0, kind, albedo, rough, wi, wo, n)
+
+
+def brdf_pdf(kind, rough, wi, wo, n):
+    """Solid-angle density of brdf_sample (pg/scene.py:287-308)."""
+    return _brdf(1, kind, None, rough, wi, wo, n)
+
+
+def brdf_sample(kind, albedo, rough, wo, n, streams):
+    """Scatter direction, pdf, valid; two draws per lane (pg/scene.py:354-380)."""
+    return _brdf(2, kind, albedo, rough, None, wo, n, streams)
+
+
+def primary_ray_dirs(cam, width, height, px, py):
+    """World ray directions through pixel centres (pg/scene.py:125-135)."""
+    import torch
+
+    from . import _lib
+    from .render import camera_abi
+    like = torch.is_tensor(px)
+    shape = tuple(np.shape(px))
+    x = _d64(px).reshape(-1).contiguous()
+    y = torch.broadcast_to(_d64(py).reshape(shape), shape).reshape(-1).contiguous()
+    out = torch.empty(x.shape[0], 3, dtype=torch.float64, device=x.device)
+    import ctypes
+    c = camera_abi(cam)
+    _lib.check(_lib.lib().pgg_primary_rays(ctypes.byref(c), int(width), int(height), x.shape[0], _lib.ptr(x),
+                                           _lib.ptr(y), _lib.ptr(out), _lib.stream_ptr()))
+    return _out(out.reshape(shape + (3,)), like)
+
+
+def project_to_pixels(cam, width, height, points):
+    """World points -> continuous pixel coordinates (pg/scene.py:138-151): (px, py, in_front)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .render import camera_abi
+    like = torch.is_tensor(points)
+    p = _d64(points, (-1, 3))
+    n = p.shape[0]
+    px = torch.empty(n, dtype=torch.float64, device=p.device)
+    py = torch.empty(n, dtype=torch.float64, device=p.device)
+    fr = torch.empty(n, dtype=torch.uint8, device=p.device)
+    c = camera_abi(cam)
+    _lib.check(_lib.lib().pgg_project(ctypes.byref(c), int(width), int(height), n, _lib.ptr(p), _lib.ptr(px),
+                                      _lib.ptr(py), _lib.ptr(fr), _lib.stream_ptr()))
+    return _out(px, like), _out(py, like), _out(fr.bool(), like)

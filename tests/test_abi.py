@@ -65,4 +65,4 @@ def test_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.Scene) == 8 + 16 + 24
     assert ctypes.sizeof(_lib.Camera) == 13 * 8
     assert ctypes.sizeof(_lib.RenderConfig) == 8 * 4 + 8
-    assert ctypes.sizeof(_lib.RenderOut) == 5 * 8
+    assert ctypes.sizeof(_lib.RenderOut) == 6 * 8
