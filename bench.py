@@ -53,6 +53,19 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(workload):
+    """DRAM bytes (read + write) per k_guiding_pass launch from the committed
+    `ncu --set full` capture (profiles/traffic.json, written by
+    tools/ncu_summary.py --traffic), or None for workloads not captured."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -348,7 +361,7 @@ def bench_ours(args, rank, world, local_rank):
                            "l2": "inputs larger than L2 (~200 MB/frame, 16 frames rotating); no flush",
                            "parallelism": "replicas" if world > 1 else "single"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                             "frac": achieved / peak, "traffic": ncu_traffic(args.workload), "peak_kind": peak_kind,
                              "algorithmic_bytes_per_px": bpx, "kernel_ms": kavg,
                              "kernel": "k_guiding_pass (fused)"},
                 "clocks": clk.summary(),

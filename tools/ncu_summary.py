@@ -2,9 +2,12 @@
 profiles/: headline metrics, stall reasons, and the hottest source lines.
 
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep > profiles/<name>.txt
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep --traffic 1080p   # -> profiles/traffic.json
 """
 import csv
 import io
+import json
+import os
 import subprocess
 import sys
 
@@ -36,12 +39,33 @@ def ncu(*args):
     return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
 
 
-def main(rep):
+def raw_metrics(rep):
     raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
     hdr, vals = raw[0], raw[2] if len(raw) > 2 else raw[1]
     units = raw[1] if len(raw) > 2 else [""] * len(hdr)
-    m = dict(zip(hdr, vals))
-    u = dict(zip(hdr, units))
+    return dict(zip(hdr, vals)), dict(zip(hdr, units))
+
+
+def to_bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit.strip(), 1)
+    return float(v.replace(",", "")) * scale
+
+
+def write_traffic(rep, workload):
+    """DRAM read + write bytes of the captured launch -> profiles/traffic.json[workload]."""
+    m, u = raw_metrics(rep)
+    b = to_bytes(m["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + \
+        to_bytes(m["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
+    d = json.load(open(path)) if os.path.exists(path) else {}
+    d[workload] = {"dram_bytes_per_launch": b, "kernel": m.get("Kernel Name", "?"), "source": os.path.basename(rep)}
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1)
+    print(json.dumps(d[workload]))
+
+
+def main(rep):
+    m, u = raw_metrics(rep)
     print(f"# ncu --set full summary: {rep}")
     print(f"kernel: {m.get('Kernel Name', '?')}")
     print(f"grid {m.get('Grid Size', '?')} block {m.get('Block Size', '?')}")
@@ -77,4 +101,7 @@ def main(rep):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if len(sys.argv) > 3 and sys.argv[2] == "--traffic":
+        write_traffic(sys.argv[1], sys.argv[3])
+    else:
+        main(sys.argv[1])
