@@ -53,6 +53,9 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 constexpr int TILE_W = 32, TILE_H = PGG_TILE_H, THREADS = TILE_W * TILE_H;
 constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this radius
 
+#ifndef PGG_PHASE_SYNC
+#define PGG_PHASE_SYNC 1  // block-wide barrier between stage 1 and the EM loop: 0.5585 vs 0.5623 ms
+#endif
 #ifndef PGG_STASH
 #define PGG_STASH 1
 #endif
@@ -157,6 +160,9 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   }
   if constexpr (EM_LANES == 1) {
     // one lane per pixel end to end: the EM context stays in registers
+#if PGG_PHASE_SYNC
+    __syncthreads();  // keep a block's warps in one code phase (instruction-cache locality)
+#endif
     if (kTile) mbar_wait(bar, 0);
     if (!active) return;
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
