@@ -37,16 +37,6 @@ using pgg_rt::g_cuda_err;
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// ---------------------------------------------------------------------------
-// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row.
-//   stage 1  lane = pixel: reproject Gamma, lobe + truncation mass, depth-0
-//            sampling, EM context -> shared memory (field-major per warp)
-//   stage 2  4 lanes per pixel, 8 pixels per round, 4 rounds: lane j of a
-//            group handles candidate slots j, j+4, j+8, ...; partial sums
-//            meet in a fixed xor-butterfly (deterministic, same order as the
-//            host build's em_combine)
-//   stage 3  lane = pixel: float64 M-step, Gamma' store
-
 #ifndef PGG_TILE_H
 #define PGG_TILE_H 8
 #endif
@@ -71,9 +61,9 @@ struct SmemLayout {
     tile_bytes = tile ? (size_t)cols * rows * 16 : 0;
     off_l = (tile_bytes + 127) & ~(size_t)127;
     off_em = off_l + ((tile_bytes + 127) & ~(size_t)127);
-    // EM_LANES == 1: the lane's Gamma (2 float4) parked during the EM loop
-    const size_t em_bytes = EM_LANES > 1 ? (size_t)TILE_H * EM_WORDS * TILE_W * 4 : (size_t)THREADS * 32;
-    const size_t sum_bytes = EM_LANES > 1 ? (size_t)TILE_H * 7 * TILE_W * 4 : 0;
+    // the lane's Gamma (2 float4) parked during the EM loop
+    const size_t em_bytes = (size_t)THREADS * 32;
+    const size_t sum_bytes = 0;
     off_sum = off_em + em_bytes;
     off_bar = off_sum + sum_bytes;
     total = off_bar + 16;
@@ -104,18 +94,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // ---------------------------------------------------------------------------
-// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row.
+// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row, one
+// lane per pixel end to end.
 //   stage 0  (kTile) one thread issues two TMA loads of the block's VPL tile
 //            plus the EM halo (Pi y and L planes) into shared memory; they
 //            land while stage 1 runs
-//   stage 1  lane = pixel: reproject Gamma, lobe + truncation mass, depth-0
-//            sampling, EM context -> shared memory (field-major per warp)
-//   stage 2  4 lanes per pixel, 8 pixels per round, 4 rounds: lane j of a
-//            group handles candidate slots j, j+4, j+8, ...; partial sums
-//            meet in a fixed xor-butterfly (deterministic, same order as the
-//            host build's em_combine)
-//   stage 3  lane = pixel: float64 M-step, Gamma' store
-// Warps never wait for each other after the start-up barrier.
+//   stage 1  reproject Gamma, lobe + truncation mass, depth-0 sampling, EM
+//            context (registers)
+//   stage 2  EM over the pixel's candidate slots, VPLs from the tile
+//   stage 3  float64 M-step, Gamma' store
+// Measured alternatives (2/4/8 lanes per pixel with a butterfly reduction,
+// a split stage-1 / EM kernel pair) were slower; see DESIGN.md section 4.
 
 template <bool kTile>
 __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
@@ -126,7 +115,6 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   float4* tile_y = reinterpret_cast<float4*>(smem);
   float4* tile_l = reinterpret_cast<float4*>(smem + SL.off_l);
   float* s_em = reinterpret_cast<float*>(smem + SL.off_em);
-  float* s_sum = reinterpret_cast<float*>(smem + SL.off_sum);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SL.off_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int band_y0 = A.cfg.row0 + blockIdx.y * TILE_H;  // frame row of the tile's first row
@@ -158,161 +146,34 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
     S.flags = 0;
     S.nb = 0;
   }
-  if constexpr (EM_LANES == 1) {
-    // one lane per pixel end to end: the EM context stays in registers
+  // one lane per pixel end to end: the EM context stays in registers
 #if PGG_PHASE_SYNC
-    __syncthreads();  // keep a block's warps in one code phase (instruction-cache locality)
+  __syncthreads();  // keep a block's warps in one code phase (instruction-cache locality)
 #endif
-    if (kTile) mbar_wait(bar, 0);
-    if (!active) return;
-    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const int y = A.cfg.row0 + yl;
-#if PGG_STASH
-    // park Gamma in shared memory: 8 registers fewer live across the EM loop
-    float4* stash = reinterpret_cast<float4*>(s_em);
-    stash[threadIdx.x] = g0;
-    stash[THREADS + threadIdx.x] = g1;
-#endif
-    if (train) {
-      if (kTile) {
-        const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
-        em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
-      } else {
-        const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
-        em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
-      }
-    }
-    const int64_t own = (int64_t)yl * A.cfg.width + x;
-#if PGG_STASH
-    g0 = stash[threadIdx.x];
-    g1 = stash[THREADS + threadIdx.x];
-#endif
-    float4 o0 = g0, o1 = g1;
-    if (train) m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
-    st4(A.gout.g0, own, o0);
-    st4(A.gout.g1, own, o1);
-    return;
-  }
-  float* my_em = s_em + warp * EM_WORDS * TILE_W;
-  em_to_words(S, my_em + lane, TILE_W);
-  __syncwarp();
-  if (kTile) mbar_wait(bar, 0);
-  const int j = lane & (EM_LANES - 1);
-  const int y = A.cfg.row0 + yl;
-  constexpr int PIX_PER_ROUND = 32 / EM_LANES;
-#pragma unroll 1
-  for (int g = 0; g < EM_LANES; ++g) {
-    const int p = PIX_PER_ROUND * g + lane / EM_LANES;
-    const EmSetup P = em_from_words(my_em + p, TILE_W);
-    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (P.flags & 1) {
-      const int px = blockIdx.x * TILE_W + p;
-      if (kTile) {
-        const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
-        em_partial(A, V, P, px, y, j, c_jmul, c_jadd, acc);
-      } else {
-        const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
-        em_partial(A, V, P, px, y, j, c_jmul, c_jadd, acc);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      float v = acc[k];
-#pragma unroll
-      for (int m = EM_LANES / 2; m >= 1; m /= 2) v += __shfl_xor_sync(0xffffffffu, v, m);
-      acc[k] = v;
-    }
-    if (j == 0) {
-#pragma unroll
-      for (int k = 0; k < 7; ++k) s_sum[(warp * 7 + k) * TILE_W + p] = acc[k];
-    }
-  }
-  __syncwarp();
-  if (!active) return;
-  const int64_t own = (int64_t)yl * A.cfg.width + x;
-  float4 o0 = g0, o1 = g1;
-  if (train) {
-    float acc[7];
-#pragma unroll
-    for (int k = 0; k < 7; ++k) acc[k] = s_sum[(warp * 7 + k) * TILE_W + lane];
-    m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
-  }
-  st4(A.gout.g0, own, o0);
-  st4(A.gout.g1, own, o1);
-}
-
-// ---------------------------------------------------------------------------
-// Split form (two launches): stage 1 (reproject, lobe, samples) writes the
-// reprojected Gamma and the 4 lobe constants of the EM; the EM kernel
-// rebuilds the rest of the EM context from the G-buffer.  The EM kernel then
-// needs ~80 registers instead of the fused kernel's 128 (3 blocks / SM).
-
-__global__ void __launch_bounds__(THREADS, 2) k_stage1(const PassArgs A, float4* __restrict__ lobe_out) {
-  const int x = blockIdx.x * TILE_W + (threadIdx.x & 31);
-  const int yl = blockIdx.y * TILE_H + (threadIdx.x >> 5);
-  if (x >= A.cfg.width || yl >= A.cfg.rows) return;
-  float4 g0, g1;
-  EmSetup S;
-  const bool train = pixel_stage(A, x, yl, g0, g1, S);
-  if (lobe_out) {
-    const int64_t own = (int64_t)yl * A.cfg.width + x;
-    lobe_out[own] = train ? f4(S.il11, S.l21, S.il22, S.gnorm) : f4(0.f, 0.f, 0.f, 0.f);
-  }
-}
-
-#ifndef PGG_EM_MIN_BLOCKS
-#define PGG_EM_MIN_BLOCKS 3
-#endif
-
-template <bool kTile>
-__global__ void __launch_bounds__(THREADS, PGG_EM_MIN_BLOCKS)
-    k_em(const PassArgs A, const float4* __restrict__ lobe_in, const __grid_constant__ CUtensorMap tmY,
-         const __grid_constant__ CUtensorMap tmL, int R) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const SmemLayout SL(R, kTile);
-  float4* tile_y = reinterpret_cast<float4*>(smem);
-  float4* tile_l = reinterpret_cast<float4*>(smem + SL.off_l);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SL.off_bar);
-  const int band_y0 = A.cfg.row0 + blockIdx.y * TILE_H;
-  if (kTile) {
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                   "r"((uint32_t)(2 * SL.tile_bytes))
-                   : "memory");
-      const int c0 = (int)(blockIdx.x * TILE_W - R) * 4;
-      const int c1 = band_y0 - R - A.vpl.row0;
-      tma_load_2d(tile_y, &tmY, c0, c1, bar);
-      tma_load_2d(tile_l, &tmL, c0, c1, bar);
-    }
-    __syncthreads();
-  }
-  const int x = blockIdx.x * TILE_W + (threadIdx.x & 31);
-  const int yl = blockIdx.y * TILE_H + (threadIdx.x >> 5);
-  const bool active = x < A.cfg.width && yl < A.cfg.rows;
-  const int64_t own = (int64_t)yl * A.cfg.width + x;
-  const int y = A.cfg.row0 + yl;
-  float4 g0 = f4(0, 0, 0, 0), g1 = f4(0, 0, 0, 0);
-  EmSetup S;
-  bool train = false;
-  if (active) {
-    g0 = ld4(A.grep.g0, own);
-    g1 = ld4(A.grep.g1, own);
-    train = em_setup_from_planes(A, x, y, g0, g1, __ldg(lobe_in + own), S);
-  }
   if (kTile) mbar_wait(bar, 0);
   if (!active) return;
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int y = A.cfg.row0 + yl;
+#if PGG_STASH
+  // park Gamma in shared memory: 8 registers fewer live across the EM loop
+  float4* stash = reinterpret_cast<float4*>(s_em);
+  stash[threadIdx.x] = g0;
+  stash[THREADS + threadIdx.x] = g1;
+#endif
   if (train) {
     if (kTile) {
       const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
-      em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
+      em_partial(A, V, S, x, y, c_jmul, c_jadd, acc);
     } else {
       const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
-      em_partial(A, V, S, x, y, 0, c_jmul, c_jadd, acc);
+      em_partial(A, V, S, x, y, c_jmul, c_jadd, acc);
     }
   }
+  const int64_t own = (int64_t)yl * A.cfg.width + x;
+#if PGG_STASH
+  g0 = stash[threadIdx.x];
+  g1 = stash[THREADS + threadIdx.x];
+#endif
   float4 o0 = g0, o1 = g1;
   if (train) m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
   st4(A.gout.g0, own, o0);
@@ -352,40 +213,7 @@ bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int
 }
 
 template <bool kTile>
-int launch_split(PassArgs A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
-  const SmemLayout SL(R, kTile);
-  static bool attr_set = false;
-  if (!attr_set) {
-    const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);
-    cudaFuncSetAttribute(k_em<kTile>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
-    attr_set = true;
-  }
-  const int64_t p = (int64_t)A.cfg.width * A.cfg.rows;
-  // stream-ordered scratch: reprojected Gamma (unless the caller wants it) and the lobe constants
-  const bool own_grep = !A.has_grep;
-  char* scratch = nullptr;
-  const size_t bytes = (size_t)p * 16 * (own_grep ? 3 : 1);
-  if (cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st) != cudaSuccess) return check_launch();
-  float4* lobe = reinterpret_cast<float4*>(scratch);
-  if (own_grep) {
-    A.grep.g0 = reinterpret_cast<float*>(scratch + (size_t)p * 16);
-    A.grep.g1 = reinterpret_cast<float*>(scratch + (size_t)p * 32);
-    A.has_grep = 1;
-  }
-  const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
-  PassArgs A1 = A;
-  A1.has_vpl = 1;  // stage 1 builds the EM constants
-  k_stage1<<<grid, THREADS, 0, st>>>(A1, lobe);
-  k_em<kTile><<<grid, THREADS, SL.total, st>>>(A, lobe, my, ml, R);
-  const int rc = check_launch();
-  cudaFreeAsync(scratch, st);
-  return rc;
-}
-
-template <bool kTile>
 int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
-  static const bool split = getenv("PGG_SPLIT") && getenv("PGG_SPLIT")[0] == '1';
-  if (split && A.has_vpl) return launch_split<kTile>(A, my, ml, R, st);
   const SmemLayout SL(R, kTile);
   static bool attr_set = false;  // opt in once to the largest layout this instantiation can use
   if (!attr_set) {

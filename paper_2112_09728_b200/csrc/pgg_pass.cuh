@@ -14,7 +14,10 @@
 namespace pgg {
 
 constexpr int SLOTS = 20;                 // guide_buffers.py:20
-constexpr int GAUSS_TRIES = 16;           // mixture.py:28
+#ifndef PGG_PROF_TRIES
+#define PGG_PROF_TRIES 16  // measurement-only override
+#endif
+constexpr int GAUSS_TRIES = PGG_PROF_TRIES;  // mixture.py:28 (16)
 constexpr uint64_t J19_MUL = pcg_jump_mul(SLOTS - 1);
 constexpr uint64_t J19_ADD = pcg_jump_add(SLOTS - 1);
 
@@ -389,53 +392,6 @@ struct EmSetup {
   int nb;            // neighbour budget N (mixture.py:324-328)
   uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
 };
-constexpr int EM_WORDS = 35;  // EmSetup serialised as 32-bit words
-
-PGG_HD void em_to_words(const EmSetup& S, float* w, int stride) {
-  const float v[31] = {S.x.x, S.x.y, S.x.z, S.fr.t.x, S.fr.t.y, S.fr.t.z, S.fr.b.x, S.fr.b.y, S.fr.b.z,
-                       S.fr.n.x, S.fr.n.y, S.fr.n.z, S.n_raw.x, S.n_raw.y, S.n_raw.z, S.wol.x, S.wol.y,
-                       S.wol.z, S.alb_r, S.alb_g, S.alb_b, S.a2, S.kappa, S.g1o, S.mx, S.my, S.il11, S.l21,
-                       S.il22, S.gnorm, S.pi};
-  for (int i = 0; i < 31; ++i) w[i * stride] = v[i];
-  const int32_t iv[2] = {S.flags, S.nb};
-  const uint32_t lo = (uint32_t)S.s0, hi = (uint32_t)(S.s0 >> 32);
-  memcpy(&w[31 * stride], &iv[0], 4);
-  memcpy(&w[32 * stride], &iv[1], 4);
-  memcpy(&w[33 * stride], &lo, 4);
-  memcpy(&w[34 * stride], &hi, 4);
-}
-
-PGG_HD EmSetup em_from_words(const float* w, int stride) {
-  EmSetup S;
-  float v[31];
-  for (int i = 0; i < 31; ++i) v[i] = w[i * stride];
-  S.x = v3(v[0], v[1], v[2]);
-  S.fr.t = v3(v[3], v[4], v[5]);
-  S.fr.b = v3(v[6], v[7], v[8]);
-  S.fr.n = v3(v[9], v[10], v[11]);
-  S.n_raw = v3(v[12], v[13], v[14]);
-  S.wol = v3(v[15], v[16], v[17]);
-  S.alb_r = v[18];
-  S.alb_g = v[19];
-  S.alb_b = v[20];
-  S.a2 = v[21];
-  S.kappa = v[22];
-  S.g1o = v[23];
-  S.mx = v[24];
-  S.my = v[25];
-  S.il11 = v[26];
-  S.l21 = v[27];
-  S.il22 = v[28];
-  S.gnorm = v[29];
-  S.pi = v[30];
-  uint32_t lo, hi;
-  memcpy(&S.flags, &w[31 * stride], 4);
-  memcpy(&S.nb, &w[32 * stride], 4);
-  memcpy(&lo, &w[33 * stride], 4);
-  memcpy(&hi, &w[34 * stride], 4);
-  S.s0 = ((uint64_t)hi << 32) | lo;
-  return S;
-}
 
 // jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..37
 // (every draw position of the 38-draw EM candidate block)
@@ -457,12 +413,7 @@ PGG_HD void jump_tables(uint64_t* mul, uint64_t* add) {
     a = a * PCG_MUL + PCG_INC;
   }
 }
-#ifndef PGG_EM_LANES
-#define PGG_EM_LANES 1  // measured on B200: 1 lane/pixel 0.757 ms, 2: 0.796, 4: 0.868, 8: 1.03 (1080p)
-#endif
-constexpr int EM_LANES = PGG_EM_LANES;  // lanes per pixel in stage 2
-constexpr uint64_t JL_MUL = pcg_jump_mul(EM_LANES);
-constexpr uint64_t JL_ADD = pcg_jump_add(EM_LANES);
+
 
 // XSH-RR output of a state (without advancing it)
 PGG_HD uint32_t pcg_out(uint64_t old) {
@@ -629,12 +580,12 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, i
   em_accumulate(S, vy, V, V.index(cx, cy), true, acc, [&]() { return S.n_raw; });
 }
 
-// Partial sums of lane j of a pixel's group: slots j, j + EM_LANES, ... < N.
-// Slot 0 is the pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and
-// u2 = draw 18+s of the pixel's stream (the reference draws all 19 u1 then
-// all 19 u2, guide_buffers.py:144-145) and rounds the disk offset.
+// EM sums of one pixel over its candidate slots 0..N-1.  Slot 0 is the
+// pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and u2 = draw 18+s of
+// the pixel's stream (the reference draws all 19 u1 then all 19 u2,
+// guide_buffers.py:144-145) and rounds the disk offset.
 template <class VS>
-PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, int j, const uint64_t* jmul,
+PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, const uint64_t* jmul,
                        const uint64_t* jadd, float* acc) {
   const pgg_config& C = A.cfg;
   const unsigned W = (unsigned)C.width, H = (unsigned)C.height;
@@ -651,29 +602,19 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     const float4 nd = ld4(A.cur.nd, (int64_t)(y - A.cur.row0) * C.width + x);
     return v3(nd.x, nd.y, nd.z);
   };
-  int s = j;
-  uint64_t sa = 0, sb = 0;
-  if (s == 0) {
+  {
     const float4 vy = V.y_at(base);
     em_accumulate(S, vy, V, base, vy.w != 0.0f, acc, n_raw);
-    s = EM_LANES;
   }
+  int s = 1;
   if (s >= S.nb) return;
-  sa = jmul[s - 1] * S.s0 + jadd[s - 1];
-  sb = jmul[s + 18] * S.s0 + jadd[s + 18];
-#ifndef PGG_EM_UNROLL
-#define PGG_EM_UNROLL 1
-#endif
-#if PGG_EM_UNROLL == 2
-#pragma unroll 2
-#elif PGG_EM_UNROLL == 3
-#pragma unroll 3
-#endif
+  uint64_t sa = jmul[0] * S.s0 + jadd[0];     // draw 0: u1 of slot 1
+  uint64_t sb = jmul[19] * S.s0 + jadd[19];   // draw 19: u2 of slot 1
   int misses = 0;  // in-frame candidates outside the supplied VPL rows (halo misses)
-  for (; s < S.nb; s += EM_LANES) {
+  for (; s < S.nb; ++s) {
     const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
-    sa = sa * JL_MUL + JL_ADD;
-    sb = sb * JL_MUL + JL_ADD;
+    sa = sa * PCG_MUL + PCG_INC;
+    sb = sb * PCG_MUL + PCG_INC;
     int dx, dy;
     disk_offset(ua, ub, C.radius, dx, dy);
     const int cx = x + dx, cy = y + dy;
@@ -687,19 +628,6 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     em_accumulate(S, vy, V, idx, ok, acc, n_raw);
   }
   if (misses) count_miss(A.halo_misses, misses);
-}
-
-// The butterfly order of the device reduction (xor EM_LANES/2, ..., 1), so
-// the host build sums in exactly the same order.
-PGG_HD void em_combine(float p[EM_LANES][7], float* out) {
-  for (int k = 0; k < 7; ++k) {
-    float v[EM_LANES];
-    for (int j = 0; j < EM_LANES; ++j) v[j] = p[j][k];
-    for (int m = EM_LANES / 2; m >= 1; m /= 2)
-      for (int j = 0; j < EM_LANES; ++j)
-        if (!(j & m)) v[j] = v[j] + v[j | m];  // lane j and j^m hold the same sum afterwards
-    out[k] = v[0];
-  }
 }
 
 // Online M-step (mixture.py:276-321) in float64 from the float32 sums.
@@ -885,50 +813,7 @@ PGG_HD void em_dump(const PassArgs& A, int x, int y, uint64_t s0, const uint64_t
   }
 }
 
-// EM context rebuilt by the split EM kernel from the G-buffer planes, the
-// reprojected Gamma and the lobe constants stage 1 stored (il11', l21',
-// il22', gnorm): the same floats the fused path keeps in registers.
-// Returns the train flag (valid pixel, view above the surface).
-PGG_HD bool em_setup_from_planes(const PassArgs& A, int x, int y, const float4& g0, const float4& g1,
-                                 const float4& lobe4, EmSetup& S) {
-  const pgg_config& C = A.cfg;
-  const int64_t ci = (int64_t)(y - A.cur.row0) * C.width + x;
-  const uint8_t fl = ldu8(A.cur.flags, ci);
-  S.flags = 0;
-  S.nb = 0;
-  if (!(fl & 1)) return false;
-  const float4 nd = ld4(A.cur.nd, ci), pr = ld4(A.cur.pr, ci), va = ld4(A.cur.va, ci), am = ld4(A.cur.am, ci);
-  const V3<float> n = v3(nd.x, nd.y, nd.z);
-  const PixelFrame pf = make_pixel_frame(n, v3(va.x, va.y, va.z));
-  if (!pf.co_pos) return false;
-  const bool glossy = (fl & 4) != 0;
-  const double r2d = (double)pr.w * (double)pr.w;
-  const float alpha = (float)fmax(r2d, 1e-6);
-  S.x = v3(pr.x, pr.y, pr.z);
-  S.fr = pf.fr;
-  S.n_raw = n;
-  S.wol = pf.wol;
-  S.alb_r = 0.2126f * va.w;
-  S.alb_g = 0.7152f * am.x;
-  S.alb_b = 0.0722f * am.y;
-  S.a2 = alpha * alpha;
-  S.kappa = kappa_world(pf.om_nn, S.a2);
-  S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
-  S.mx = g0.x;
-  S.my = g0.y;
-  S.il11 = lobe4.x;
-  S.l21 = lobe4.y;
-  S.il22 = lobe4.z;
-  S.gnorm = lobe4.w;
-  S.pi = g1.z;
-  S.flags = 1 | (glossy ? 2 : 0) | 4;
-  S.nb = neighbor_budget(g1.w, C.k_max);
-  S.s0 = pcg_lane(C.key_train, (uint64_t)y * (uint64_t)C.width + (uint64_t)x);
-  return true;
-}
-
-// Whole pixel on one thread (host build): the device splits stage 2 over a
-// 4-lane group; this runs the same partitions and reduction order serially.
+// Whole pixel on one thread (host build of the device code path).
 PGG_HD void pass_pixel(const PassArgs& A, int x, int yl, const uint64_t* jmul, const uint64_t* jadd) {
   float4 g0, g1;
   EmSetup S;
@@ -937,14 +822,9 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl, const uint64_t* jmul, c
   const int64_t own = (int64_t)yl * A.cfg.width + x;
   float4 o0 = g0, o1 = g1;
   if (train) {
-    float p[EM_LANES][7];
+    float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
-    for (int j = 0; j < EM_LANES; ++j) {
-      for (int k = 0; k < 7; ++k) p[j][k] = 0.0f;
-      em_partial(A, V, S, x, A.cfg.row0 + yl, j, jmul, jadd, p[j]);
-    }
-    float acc[7];
-    em_combine(p, acc);
+    em_partial(A, V, S, x, A.cfg.row0 + yl, jmul, jadd, acc);
     m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
   }
   st4(A.gout.g0, own, o0);
