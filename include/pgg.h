@@ -139,6 +139,19 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
                      const pgg_gamma_out* gamma_out, const pgg_samples* samples, int32_t* halo_misses,
                      void* stream);
 
+/* One stage of the pass each (= pgg_guiding_pass with that stage only):
+ *   pgg_reproject ............ guide_buffers.reproject (guide_buffers.py:78-137)
+ *   pgg_train ................ guide_buffers.training_pass (guide_buffers.py:262-283)
+ *                              on an already reprojected Gamma
+ *   pgg_sample_first_bounce .. the render's depth-0 sampling (ptrace.py:161-220,
+ *                              449-475) for every pixel x spp lane */
+int pgg_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                  const pgg_gamma_in* gamma_prev, const pgg_gamma_out* gamma_out, int32_t* halo_misses, void* stream);
+int pgg_train(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma, const pgg_vpl* vpl,
+              const pgg_gamma_out* gamma_out, int32_t* halo_misses, void* stream);
+int pgg_sample_first_bounce(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma,
+                            const pgg_samples* samples, void* stream);
+
 /* Training records of n pixels (pix_xy: n x int32 (x, y)) for
  * guide_buffers.gather_training_batch (guide_buffers.py:234-259): the EM
  * candidate draws come from the caller's per-pixel PCG32 states (states is

@@ -78,6 +78,12 @@ _SIGS = {
     "pgg_guiding_pass": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GBuffer),
                          ctypes.POINTER(GammaIn), ctypes.POINTER(Vpl), ctypes.POINTER(GammaOut),
                          ctypes.POINTER(GammaOut), ctypes.POINTER(Samples), c_p, c_p],
+    "pgg_reproject": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GBuffer), ctypes.POINTER(GammaIn),
+                      ctypes.POINTER(GammaOut), c_p, c_p],
+    "pgg_train": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GammaIn), ctypes.POINTER(Vpl),
+                  ctypes.POINTER(GammaOut), c_p, c_p],
+    "pgg_sample_first_bounce": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GammaIn),
+                                ctypes.POINTER(Samples), c_p],
     "pgg_train_records": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GammaIn),
                           ctypes.POINTER(Vpl), c_i64, c_p, c_p, c_p, c_p],
     "pgg_sample_lanes": [c_i64, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],

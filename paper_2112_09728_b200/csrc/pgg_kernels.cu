@@ -500,6 +500,26 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   return launch_pass<false>(A, my, ml, 0, S(stream));
 }
 
+// Single-stage conveniences over the fused pass (the entry points SURVEY 8b
+// names): each is pgg_guiding_pass with one stage selected.
+int pgg_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                  const pgg_gamma_in* gamma_prev, const pgg_gamma_out* gamma_out, int32_t* halo_misses, void* stream) {
+  if (!prev || !gamma_out) return PGG_ERR_ARGUMENT;
+  return pgg_guiding_pass(cfg, cur, prev, gamma_prev, nullptr, gamma_out, nullptr, nullptr, halo_misses, stream);
+}
+
+int pgg_train(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma, const pgg_vpl* vpl,
+              const pgg_gamma_out* gamma_out, int32_t* halo_misses, void* stream) {
+  if (!vpl || !gamma_out) return PGG_ERR_ARGUMENT;
+  return pgg_guiding_pass(cfg, cur, nullptr, gamma, vpl, nullptr, gamma_out, nullptr, halo_misses, stream);
+}
+
+int pgg_sample_first_bounce(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma,
+                            const pgg_samples* samples, void* stream) {
+  if (!samples) return PGG_ERR_ARGUMENT;
+  return pgg_guiding_pass(cfg, cur, nullptr, gamma, nullptr, nullptr, nullptr, samples, nullptr, stream);
+}
+
 int pgg_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gamma_in* gamma, const pgg_vpl* vpl,
                       int64_t n, const int32_t* pix_xy, const uint64_t* states, float* records, void* stream) {
   if (!cfg || !cur || !gamma || !vpl || n < 0 || !pix_xy || !states || !records || cfg->k_max < 1)
