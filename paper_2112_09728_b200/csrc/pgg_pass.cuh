@@ -18,6 +18,8 @@ constexpr int SLOTS = 20;                 // guide_buffers.py:20
 #define PGG_PROF_TRIES 16  // measurement-only override
 #endif
 constexpr int GAUSS_TRIES = PGG_PROF_TRIES;  // mixture.py:28 (16)
+constexpr uint64_t J3_MUL = pcg_jump_mul(3);
+constexpr uint64_t J3_ADD = pcg_jump_add(3);
 constexpr uint64_t J19_MUL = pcg_jump_mul(SLOTS - 1);
 constexpr uint64_t J19_ADD = pcg_jump_add(SLOTS - 1);
 
@@ -751,7 +753,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     cd.from_floats = 0;
     for (int s = 0; s < C.spp; ++s) {
       uint64_t st = pcg_lane(C.key_sample, pix * (uint64_t)C.spp + (uint64_t)s);
-      for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
+      if (C.nee_draws == 3) {
+        st = st * J3_MUL + J3_ADD;  // the three NEE draws as one jump
+      } else {
+        for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
+      }
       const LaneOut o = sample_lane(pf, glossy, rough, guided, L, cd, st);
       st4(A.smp.dir, own * C.spp + s, f4(o.wi.x, o.wi.y, o.wi.z, o.pdf));
       A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
