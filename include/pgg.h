@@ -292,8 +292,9 @@ int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n,
 /* Image error (metrics.mse / metrics.rel_mse, metrics.py:24-38) of n
  * float32 elements: mean of (a - ref)^2, or of (a - ref)^2 / (ref^2 + 0.01)
  * when relative != 0, accumulated in float64 with a fixed reduction order
- * (deterministic).  scratch: 592 doubles of device memory; out: one double
- * (device). */
+ * (deterministic).  scratch: PGG_IMAGE_ERROR_SCRATCH doubles of device
+ * memory; out: one double (device). */
+#define PGG_IMAGE_ERROR_SCRATCH 1184
 int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relative, double* scratch, double* out,
                     void* stream);
 

@@ -15,6 +15,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PGG_LIB") or os.path.join(_HERE, "libpgg.so")  # PGG_LIB: A/B builds
 
 
+IMAGE_ERROR_SCRATCH = 1184  # PGG_IMAGE_ERROR_SCRATCH (include/pgg.h)
+
+
 class PggUnavailable(RuntimeError):
     """libpgg.so or a CUDA device is missing (there is no CPU fallback)."""
 

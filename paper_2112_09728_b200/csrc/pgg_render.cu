@@ -573,7 +573,13 @@ __global__ void __launch_bounds__(RT_W * RT_H, PGG_RENDER_MIN_BLOCKS) k_render(c
 // Image error metrics (pg/metrics.py:24-47): float64 per-element terms,
 // deterministic two-level reduction (fixed grid, fixed tree), no atomics.
 
-constexpr int ERR_BLOCKS = 592;  // 4 x 148 SMs
+#ifndef PGG_ERR_UNROLL
+#define PGG_ERR_UNROLL 1
+#endif
+#ifndef PGG_ERR_GRID
+#define PGG_ERR_GRID PGG_IMAGE_ERROR_SCRATCH
+#endif
+constexpr int ERR_BLOCKS = PGG_ERR_GRID;  // 8 x 148 SMs, one partial per block
 constexpr int ERR_THREADS = 256;
 
 __device__ __forceinline__ double err_term(float a, float r, int rel) {
@@ -582,6 +588,10 @@ __device__ __forceinline__ double err_term(float a, float r, int rel) {
   if (!rel) return e;
   const double rr = (double)r;
   return e / (rr * rr + 0.01);
+}
+
+__device__ __forceinline__ double err4(const float4& x, const float4& y, int rel) {
+  return ((err_term(x.x, y.x, rel) + err_term(x.y, y.y, rel)) + err_term(x.z, y.z, rel)) + err_term(x.w, y.w, rel);
 }
 
 __device__ double block_sum(double v, double* sh) {
@@ -597,22 +607,32 @@ __device__ double block_sum(double v, double* sh) {
   return v;
 }
 
+// HBM-bound: 8 bytes read per element.  Four independent float4 pairs are
+// loaded per step so each thread keeps several requests in flight.
 __global__ void __launch_bounds__(ERR_THREADS) k_err_partial(int64_t n, const float* __restrict__ a,
                                                             const float* __restrict__ r, int rel, double* part) {
   __shared__ double sh[32];
   double acc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // 4 float4 per step when aligned: the pass is HBM-bound (8 B read per element)
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n4 = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(r)) & 15) ? 0 : n / 4;
   const float4* a4 = reinterpret_cast<const float4*>(a);
   const float4* r4 = reinterpret_cast<const float4*>(r);
-  for (; i < n4; i += stride) {
-    const float4 x = a4[i], y = r4[i];
-    acc += ((err_term(x.x, y.x, rel) + err_term(x.y, y.y, rel)) + err_term(x.z, y.z, rel)) + err_term(x.w, y.w, rel);
+  int64_t i = t0;
+#if PGG_ERR_UNROLL
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const float4 x0 = __ldcs(a4 + i), y0 = __ldcs(r4 + i);
+    const float4 x1 = __ldcs(a4 + i + stride), y1 = __ldcs(r4 + i + stride);
+    const float4 x2 = __ldcs(a4 + i + 2 * stride), y2 = __ldcs(r4 + i + 2 * stride);
+    const float4 x3 = __ldcs(a4 + i + 3 * stride), y3 = __ldcs(r4 + i + 3 * stride);
+    acc += err4(x0, y0, rel);
+    acc += err4(x1, y1, rel);
+    acc += err4(x2, y2, rel);
+    acc += err4(x3, y3, rel);
   }
-  for (int64_t j = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
-    acc += err_term(a[j], r[j], rel);
+#endif
+  for (; i < n4; i += stride) acc += err4(a4[i], r4[i], rel);
+  for (int64_t j = n4 * 4 + t0; j < n; j += stride) acc += err_term(a[j], r[j], rel);
   const double s = block_sum(acc, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }

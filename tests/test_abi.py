@@ -66,3 +66,11 @@ def test_struct_layout_matches_header():
     assert ctypes.sizeof(_lib.Camera) == 13 * 8
     assert ctypes.sizeof(_lib.RenderConfig) == 8 * 4 + 8
     assert ctypes.sizeof(_lib.RenderOut) == 6 * 8
+
+
+def test_header_constants_match_binding():
+    import re
+    from paper_2112_09728_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "pgg.h")).read()
+    assert int(re.search(r"#define PGG_IMAGE_ERROR_SCRATCH (\d+)", src).group(1)) == _lib.IMAGE_ERROR_SCRATCH
+    assert int(re.search(r"#define PGG_ABI_VERSION (\d+)", src).group(1)) == 2

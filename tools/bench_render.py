@@ -86,6 +86,27 @@ def main():
            "rays_per_s_render": (seg + px * a.spp * 3) / (ms["render"] * 1e-3),  # scatter + NEE shadow (upper) rays
            "config": {"scene": a.scene, "width": a.width, "height": a.height, "spp": a.spp, "max_depth": 4,
                       "frames": a.frames, "warmup": a.warmup}}
+    # image-error kernel (metrics.rel_mse): HBM-bound reduction over two float32 images
+    from paper_2112_09728_b200 import _lib
+    img = rp.image
+    ref = img.flip(0).contiguous()
+    n = img.numel()
+    scratch = torch.empty(_lib.IMAGE_ERROR_SCRATCH, dtype=torch.float64, device=img.device)
+    res = torch.empty(1, dtype=torch.float64, device=img.device)
+    big = torch.empty(64 << 20, dtype=torch.float32, device=img.device)  # 256 MB L2 flush
+    times = []
+    for it in range(12):
+        big.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(_lib.lib().pgg_image_error(n, _lib.ptr(img), _lib.ptr(ref), 1, _lib.ptr(scratch), _lib.ptr(res),
+                                              _lib.stream_ptr()))
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+    t = sorted(times)[len(times) // 2]
+    out["image_error"] = {"ms": t, "GB/s": 8.0 * n / (t * 1e-3) / 1e9, "bytes": 8 * n}
     if a.cpu_sample:
         from types import SimpleNamespace
 
