@@ -143,16 +143,8 @@ class RenderResult:
 
 
 def _device_scene(scene):
-    from .render import DeviceScene
-    dev = _conv.device()
-    cached = getattr(scene, "_pgg_device_scene", None)
-    if cached is None or cached.device != dev:
-        cached = DeviceScene(scene, dev)
-        try:
-            scene._pgg_device_scene = cached
-        except AttributeError:
-            pass
-    return cached
+    from .render import device_scene
+    return device_scene(scene, _conv.device())
 
 
 def gbuffer_from_planes(fgb, cam_origin):

@@ -27,9 +27,10 @@ from .layout import GBufferPlanes, SamplePlanes, VplPlanes
 class DeviceScene:
     """A Scene's packed float64 table resident on the device (pgg_scene)."""
 
-    def __init__(self, scene, device=None):
+    def __init__(self, scene, device=None, packed=None):
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        table, (nm, ns, nq, ne) = scene.pack()
+        table, (nm, ns, nq, ne) = packed if packed is not None else scene.pack()
+        self.key = table.tobytes()
         self.scene = scene
         self.table = torch.from_numpy(table).to(dev)
         self.abi = _lib.Scene(_lib.ptr(self.table), nm, ns, nq, ne)
@@ -37,6 +38,20 @@ class DeviceScene:
             self.abi.background[i] = float(scene.background[i])
         self.num_emitters = ne
         self.device = dev
+
+
+def device_scene(scene, device):
+    """The scene's device table, cached on the Scene object and rebuilt when
+    the scene's contents (or the device) change."""
+    packed = scene.pack()
+    ds = getattr(scene, "_pgg_device_scene", None)
+    if ds is None or ds.device != device or ds.key != packed[0].tobytes():
+        ds = DeviceScene(scene, device, packed)
+        try:
+            scene._pgg_device_scene = ds
+        except AttributeError:
+            pass
+    return ds
 
 
 def camera_abi(cam):

@@ -426,13 +426,8 @@ def _out(t, like_torch):
 
 
 def _device_scene(scene):
-    from .render import DeviceScene
-    dev = _dev()
-    ds = getattr(scene, "_pgg_device_scene", None)
-    if ds is None or ds.device != dev:
-        ds = DeviceScene(scene, dev)
-        scene._pgg_device_scene = ds
-    return ds
+    from .render import device_scene
+    return device_scene(scene, _dev())
 
 
 def _states_in(streams):

@@ -137,3 +137,16 @@ def test_trace_pixel_matches_frame_lane(cuda_dev):
             else:
                 np.testing.assert_array_equal(color.astype(np.float32), full.image[y, x])
             assert vpl["valid"] == bool(full.vpl.valid[y, x])
+
+
+def test_device_table_follows_scene_edits(cuda_dev):
+    """The cached device copy of a scene is rebuilt when the scene changes."""
+    from paper_2112_09728_b200 import scene as S
+    sc = _scene()
+    o, d = _rays(4000, 9)
+    a = S.intersect(sc, o, d)
+    sc.sph_radius = sc.sph_radius * 1.5
+    b = S.intersect(sc, o, d)
+    ref = RO.cast(sc, o, d)
+    assert (b["hit"] == ref.hit).mean() >= 0.9999 and (b["mat"] == ref.mat).mean() >= 0.9999
+    assert not np.array_equal(a["t"], b["t"])
