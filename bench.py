@@ -143,6 +143,42 @@ def make_frames(dev, spp, seed=0):
     return frames
 
 
+def workload_stats(frames, gamma):
+    """SURVEY 8(d) reporting: invalid-pixel and history fractions of the
+    synthetic frames, and the lobe-reset fraction (lambda_min < 1e-6) of the
+    final Gamma over valid pixels (pgg_lobe's reset flags)."""
+    import torch
+
+    from paper_2112_09728_b200 import _lib
+    fl = torch.stack([g.flags for g, _ in frames])
+    valid = (fl & 1).bool()
+    hist = ((fl & 3) == 3)
+    st = gamma.to_aos().reshape(-1, 8).to(torch.float64).contiguous()
+    n = st.shape[0]
+    dev = st.device
+    e = lambda *s: torch.empty(*s, dtype=torch.float64, device=dev)  # noqa: E731
+    reset = torch.empty(n, dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().pgg_lobe(n, _lib.ptr(st), _lib.ptr(e(n, 2)), _lib.ptr(e(n, 4)), _lib.ptr(e(n, 4)),
+                                   _lib.ptr(e(n)), _lib.ptr(reset), _lib.stream_ptr()))
+    v_last = valid[(len(frames) - 1)].reshape(-1)
+    return {"invalid_fraction": round(1.0 - valid.float().mean().item(), 4),
+            "history_fraction": round(hist.float().mean().item() / max(valid.float().mean().item(), 1e-9), 4),
+            "reset_fraction": round(reset.bool()[v_last].float().mean().item(), 4)}
+
+
+def cpu_host():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count()}
+
+
 def cpu_sample_rows(threads):
     return 32 * threads
 
@@ -175,13 +211,28 @@ def run_cpu_reference(rows_per_thread=32, threads=None, frame=5, seed=0):
         return SimpleNamespace(**{k: (v[r0:r1] if isinstance(v, np.ndarray) and v.ndim >= 2 and v.shape[0] == h
                                       else v) for k, v in vars(n).items()})
 
+    stages = {"reproject": 0.0, "sample": 0.0, "train": 0.0}
+
     def band(i):
         r0, r1 = i * rows_per_thread, (i + 1) * rows_per_thread
-        O.guiding_frame(st[r0:r1], cut(gpn, r0, r1), cut(gcn, r0, r1), cut(vcn, r0, r1), seed, frame)
+        gp_, gc_, vc_ = cut(gpn, r0, r1), cut(gcn, r0, r1), cut(vcn, r0, r1)
+        t0 = time.perf_counter()
+        g = O.reproject(st[r0:r1], gp_, gc_)           # guide_buffers.reproject
+        t1 = time.perf_counter()
+        O.sample_frame(g, gc_, seed, frame)              # lobe_from_stats + _sample_first_bounce
+        t2 = time.perf_counter()
+        O.train(g, vc_, gc_, seed=seed, frame=frame)     # training_pass
+        t3 = time.perf_counter()
+        if threads == 1:
+            stages["reproject"] += t1 - t0
+            stages["sample"] += t2 - t1
+            stages["train"] += t3 - t2
 
     t = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(band, range(threads)))
+    if threads == 1:
+        run_cpu_reference.last_stages = {k: round(v, 3) for k, v in stages.items()}
     return W * h, time.perf_counter() - t, threads
 
 
@@ -339,6 +390,7 @@ def bench_ours(args, rank, world, local_rank):
     kavg = statistics.mean(kern_ms)
     achieved = bpx * W * H / (kavg * 1e-3) / 1e9
 
+    wstats = workload_stats(frames, state["g"]) if rank == 0 else {}
     e2e = None
     if not args.no_e2e:
         e2e = bench_e2e(args, frames, cfg, dev, world)
@@ -347,7 +399,8 @@ def bench_ours(args, rank, world, local_rank):
         px, secs, thr = run_cpu_reference(rows_per_thread=160, threads=1)
         cpu = {"value": px / secs / 1e6, "unit": "Mpixels/s", "cores": thr, "kind": "port",
                "sample": f"one 1920x160 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
-                         f"sampling + training_pass, oracle port of pgtrace on 1 core"}
+                         f"sampling + training_pass, oracle port of pgtrace on 1 core",
+               "stage_seconds": getattr(run_cpu_reference, "last_stages", None), **cpu_host()}
     if rank == 0:
         metric = ("guiding-pass Mpixels/s at 1080p" if args.workload == "1080p"
                   else f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)")
@@ -359,7 +412,7 @@ def bench_ours(args, rank, world, local_rank):
                                        "per frame (BASELINE %s); N>1 = N independent streams"
                                        % (W, H, args.spp, WORKLOADS[args.workload][3].split(":")[0]),
                            "l2": "inputs larger than L2 (~200 MB/frame, 16 frames rotating); no flush",
-                           "parallelism": "replicas" if world > 1 else "single"},
+                           "parallelism": "replicas" if world > 1 else "single", **wstats},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": ncu_traffic(args.workload), "peak_kind": peak_kind,
                              "algorithmic_bytes_per_px": bpx, "kernel_ms": kavg,
