@@ -53,17 +53,43 @@ def parse():
     return ap.parse_args()
 
 
-def ncu_traffic(workload):
-    """DRAM bytes (read + write) per k_guiding_pass launch from the committed
-    `ncu --set full` capture (profiles/traffic.json, written by
-    tools/ncu_summary.py --traffic), or None for workloads not captured."""
+def ncu_capture(workload, key):
+    """Per-launch figure of k_guiding_pass from the committed `ncu --set full`
+    capture (profiles/traffic.json, written by tools/ncu_summary.py
+    --traffic): DRAM bytes read + written, or warp instructions issued."""
     p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        return d.get(workload, {}).get(key)
     except (OSError, ValueError):
         return None
+
+
+def ncu_traffic(workload):
+    return ncu_capture(workload, "dram_bytes_per_launch")
+
+
+def issue_roofline(workload, kernel_ms):
+    """The bound that actually binds this kernel: warp-instruction issue.
+    achieved = ncu's warp instructions per launch / the live kernel time;
+    peak = 4 schedulers x SMs x max SM clock (one warp-instruction per
+    scheduler per cycle)."""
+    inst = ncu_capture(workload, "warp_instructions_per_launch")
+    if not inst:
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except (OSError, ValueError):
+        pass
+    achieved = inst / (kernel_ms * 1e-3) / 1e9
+    peak = 4 * sms * mhz * 1e6 / 1e9
+    return {"achieved": achieved, "peak": peak, "unit": "G warp-inst/s", "frac": achieved / peak,
+            "warp_instructions_per_launch": inst}
 
 
 def peaks():
@@ -416,6 +442,7 @@ def bench_ours(args, rank, world, local_rank):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": ncu_traffic(args.workload), "peak_kind": peak_kind,
                              "algorithmic_bytes_per_px": bpx, "kernel_ms": kavg,
+                             "issue": issue_roofline(args.workload, kavg),
                              "kernel": "k_guiding_pass (fused)"},
                 "clocks": clk.summary(),
                 "gpu_launches": args.steps,

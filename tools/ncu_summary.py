@@ -58,7 +58,9 @@ def write_traffic(rep, workload):
         to_bytes(m["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
-    d[workload] = {"dram_bytes_per_launch": b, "kernel": m.get("Kernel Name", "?"), "source": os.path.basename(rep)}
+    d[workload] = {"dram_bytes_per_launch": b, "warp_instructions_per_launch":
+                   float(m["smsp__inst_executed.sum"].replace(",", "")) if "smsp__inst_executed.sum" in m else None,
+                   "kernel": m.get("Kernel Name", "?"), "source": os.path.basename(rep)}
     with open(path, "w") as f:
         json.dump(d, f, indent=1)
     print(json.dumps(d[workload]))
