@@ -171,3 +171,44 @@ def test_render_band_split_bitwise(cuda_dev):
     assert torch.equal(torch.cat([a.vpl.y, b.vpl.y]), full.vpl.y)
     assert torch.equal(torch.cat([a.vpl.L, b.vpl.L]), full.vpl.L)
     assert int(a.counters[0] + b.counters[0]) == int(full.counters[0])
+
+
+@pytest.mark.parametrize("kind", ["sky_spheres", "sky_mixed"])
+def test_render_background_lit_scenes(cuda_dev, kind):
+    """No emitters (NEE off, background light only) and a spheres-only scene:
+    pt render vs the oracle, pg render vs the oracle within the pg policy."""
+    from oracle import pgg_render_oracle as RO
+    from paper_2112_09728_b200 import ptrace
+    from paper_2112_09728_b200 import scene as S
+    doc = {
+        "materials": [{"name": "a", "kind": "diffuse", "albedo": [0.6, 0.5, 0.4]},
+                      {"name": "g", "kind": "glossy", "albedo": [0.9, 0.9, 0.8], "roughness": 0.3}],
+        "primitives": [{"type": "sphere", "center": [0, 0, 4], "radius": 1.0, "material": "a"},
+                       {"type": "sphere", "center": [1.6, 0.3, 5], "radius": 0.8, "material": "g"},
+                       {"type": "sphere", "center": [0, -101, 4], "radius": 100.0, "material": "a"}],
+        "camera": [{"frame": 0, "origin": [0, 0.2, 0], "look_at": [0.2, 0, 4], "up": [0, 1, 0], "fov_deg": 55}],
+        "background": [0.8, 0.9, 1.0],
+    }
+    if kind == "sky_mixed":
+        doc["primitives"].append({"type": "quad", "corner": [-2, -1, 7], "edge_u": [4, 0, 0], "edge_v": [0, 3, 0],
+                                  "material": "g"})
+    sc = S.scene_from_dict(doc)
+    assert sc.num_emitters == 0
+    w, h, fr, seed = 64, 48, 0, 5
+    gb = ptrace.gbuffer_pass(sc, fr, (w, h))
+    og = SimpleNamespace(**vars(gb))
+    rng = np.random.default_rng(1)
+    stats = np.zeros((h, w, 8), np.float32)
+    stats[..., 0:2] = rng.uniform(0.3, 0.7, (h, w, 2))
+    stats[..., 2:4] = stats[..., 0:2] ** 2 + 0.02
+    stats[..., 4] = stats[..., 0] * stats[..., 1]
+    stats[..., 6] = 0.5
+    stats[..., 7] = 2
+    for mode in ("pt", "pg"):
+        cfg = ptrace.PathConfig(spp=2, guiding=(mode == "pg"))
+        st = stats if mode == "pg" else None
+        r = ptrace.render_frame(sc, fr, st, cfg, seed, gbuf=gb)
+        o = RO.render(sc, fr, seed, og, spp=2, stats=st)
+        tol, frac = (1e-6, 0.995) if mode == "pt" else (1e-4, 0.97)
+        assert _pix_close(r.image, o["image"], tol).mean() >= frac, mode
+        assert abs(r.mean_path_length - o["mean_path_length"]) <= 0.02
