@@ -46,6 +46,9 @@ constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this ra
 #ifndef PGG_PHASE_SYNC
 #define PGG_PHASE_SYNC 1  // block-wide barrier between stage 1 and the EM loop: 0.5585 vs 0.5623 ms
 #endif
+#ifndef PGG_TILE_S
+#define PGG_TILE_S 1
+#endif
 #ifndef PGG_STASH
 #define PGG_STASH 1
 #endif
@@ -162,7 +165,11 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
 #endif
   if (train) {
     if (kTile) {
+#if PGG_TILE_S
+      const VplTileS V{smem_u32(tile_y), (uint32_t)SL.off_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
+#else
       const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
+#endif
       em_partial(A, V, S, x, y, c_jmul, c_jadd, acc);
     } else {
       const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};

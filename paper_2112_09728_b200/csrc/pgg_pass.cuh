@@ -457,6 +457,31 @@ struct VplTile {
   PGG_MHD float4 L_at(int i) const { return L[i]; }
 };
 
+// The same tile through 32-bit shared-memory addresses (ld.shared.v4): one
+// base register instead of two generic pointers, L at a fixed offset.
+// Device-only (the host build reads VplGlobal).
+struct VplTileS {
+  uint32_t y;      // shared address of tile element (0, 0) of the y plane
+  uint32_t off_l;  // byte offset of the L plane
+  int x0, y0, cols;
+  PGG_MHD static float4 lds(uint32_t a) {
+    float4 v;
+#ifdef __CUDA_ARCH__
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+#else
+    (void)a;
+    v = float4{0.f, 0.f, 0.f, 0.f};
+#endif
+    return v;
+  }
+  PGG_MHD int index(int cx, int cy) const { return (cy - y0) * cols + (cx - x0); }
+  PGG_MHD int stride() const { return cols; }
+  PGG_MHD float4 y_at(int i) const { return lds(y + 16u * (uint32_t)i); }
+  PGG_MHD float4 L_at(int i) const { return lds(y + off_l + 16u * (uint32_t)i); }
+  PGG_MHD float4 get_y(int cx, int cy) const { return y_at(index(cx, cy)); }
+  PGG_MHD float4 get_L(int cx, int cy) const { return L_at(index(cx, cy)); }
+};
+
 // One training record (guide_buffers.py:186-230): receiver S, VPL (y, L).
 // Returns the reference's geometric validity (dist > 1e-9, cos > 1e-9) and
 // fills w (luminance weight), r (E-step responsibility) and the square
