@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--workload", default="1080p", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-frame-loop", action="store_true")
     return ap.parse_args()
 
 
@@ -417,6 +418,9 @@ def bench_ours(args, rank, world, local_rank):
     achieved = bpx * W * H / (kavg * 1e-3) / 1e9
 
     wstats = workload_stats(frames, state["g"]) if rank == 0 else {}
+    floop = None
+    if rank == 0 and world == 1 and args.workload == "1080p" and not args.no_frame_loop:
+        floop = bench_frame_loop(dev)
     e2e = None
     if not args.no_e2e:
         e2e = bench_e2e(args, frames, cfg, dev, world)
@@ -446,8 +450,37 @@ def bench_ours(args, rank, world, local_rank):
                              "kernel": "k_guiding_pass (fused)"},
                 "clocks": clk.summary(),
                 "gpu_launches": args.steps,
-                "e2e": e2e, "cpu_baseline": cpu}
+                "e2e": e2e, "cpu_baseline": cpu, "frame_loop": floop}
         print(json.dumps(line), flush=True)
+
+
+def bench_frame_loop(dev, frames=16, warmup=4):
+    """The whole guided frame on the GPU: G-buffer +
+    motion, reproject + depth-0 samples, NEE path lanes writing the VPLs, EM
+    (cli.RenderSession on cornell-occluder with a panning camera, 1080p,
+    1 spp).  Reported beside the headline; not part of `value`."""
+    import torch
+
+    from paper_2112_09728_b200 import cli
+    from paper_2112_09728_b200 import scene as S
+    doc = S.BUILTIN_SCENES["cornell-occluder"]()
+    k0 = dict(doc["camera"][0])
+    doc["camera"] = [k0, dict(k0, frame=1000, origin=[k0["origin"][0] + 0.3, k0["origin"][1], k0["origin"][2]])]
+    sess = cli.RenderSession(S.scene_from_dict(doc), cli.RunConfig(width=W, height=H, spp=1, mode="pg"),
+                             device=dev)
+    for f in range(warmup):
+        sess.run_frame(f)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for f in range(warmup, warmup + frames):
+        r = sess.run_frame(f)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / frames
+    return {"scene": "cornell-occluder (panning)", "ms_per_frame": ms, "Mpixels/s": W * H / (ms * 1e-3) / 1e6,
+            "mean_path_length": r.mean_path_length, "frames": frames,
+            "kernels": "k_gbuffer, k_guiding_pass (reproject+sample), k_render, k_guiding_pass (EM)"}
 
 
 def bench_e2e(args, frames, cfg, dev, world):
