@@ -85,6 +85,26 @@ def halo_exchange(tensors, ext, rank, world, group=None, tag=0):
         req.wait()
 
 
+def gather_rows(tensors, rank, world, height, group=None):
+    """All-gather of every rank's own row band (bands of unequal height are
+    padded to the largest) into full-height tensors, in row order."""
+    import torch
+    base, rem = divmod(height, world)
+    mx = base + (1 if rem else 0)
+    out = []
+    for t in tensors:
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)  # NCCL on GPUs, gloo in the CPU tests
+        full = torch.empty((height,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        for r in range(world):
+            r0, r1 = band_rows(height, world, r)
+            full[r0:r1] = parts[r][:r1 - r0]
+        out.append(full)
+    return out
+
+
 def check_band_geometry(height, world, halo):
     """Every band must be at least `halo` rows tall so that a halo comes from
     the adjacent rank only."""
@@ -176,7 +196,30 @@ class BandedGuiding:
                         height=self.H, row0=a, rows=b - a, out_gamma=out_view, out_samples=smp,
                         halo_misses=self._miss)
 
-    def step(self, frame, exchange=True, gbuf=None, vpl=None, overlap=True, split=None):
+    def history_own(self):
+        """This band's own rows of what reprojection reads from other bands:
+        previous gate planes (flags, normal+depth) and the current Gamma."""
+        eg = self.ext_g
+        g_in = self.gamma[self.cur]
+        prev = self.prev_gb
+        return [eg.own(prev.flags), eg.own(prev.nd), eg.own(g_in.g0), eg.own(g_in.g1)]
+
+    def _full_history_rerun(self, frame, cur_band, vpl, g_out, full):
+        """Re-run the band with the whole previous frame as reprojection
+        source (flags, nd, g0, g1 full-height), for motion beyond the halo."""
+        from .layout import GammaPlanes, GBufferPlanes
+        from .session import run_pass
+        flags, nd, g0, g1 = full
+        prev = GBufferPlanes(flags, nd, nd, nd, nd, self.prev_gb.cam_origin, row0=0)  # only flags / nd are read
+        gin = GammaPlanes(g0, g1, row0=0)
+        eg = self.ext_g
+        out_view = type(g_out)(eg.own(g_out.g0), eg.own(g_out.g1), row0=self.r0)
+        self._miss.zero_()
+        run_pass(self.cfg, frame, cur_band, gin, prev=prev, vpl=vpl, height=self.H, row0=self.r0,
+                 rows=self.r1 - self.r0, out_gamma=out_view, out_samples=self.samples, halo_misses=self._miss)
+
+    def step(self, frame, exchange=True, gbuf=None, vpl=None, overlap=True, split=None, fallback=False,
+             gather=None, any_miss=None):
         """Exchange halos (unless the caller already filled them, exchange=False)
         and run the fused pass on this band.  ``gbuf``/``vpl``: this frame's
         extended planes (own rows filled); default: the internal buffers.
@@ -184,7 +227,14 @@ class BandedGuiding:
         overlap=True: the grouped send/recv is posted first, the
         interior rows run while it is in flight, and the edge rows after the
         stream has waited on it; overlap=False runs exchange, then one launch.
-        split=True/False forces the interior/edge launches on or off."""
+        split=True/False forces the interior/edge launches on or off.
+
+        fallback=True handles motion beyond the halo: if any rank
+        counted a reprojection halo miss this frame (``any_miss``, default an
+        all-reduce MAX), every rank all-gathers the previous frame's gate
+        planes and Gamma (``gather``, default gather_rows) and re-runs its
+        band with the whole frame as source, which restores the 1-GPU result.
+        It costs one host sync per frame."""
         from .session import PassResult
         cur = self.gb[self.cur] if gbuf is None else gbuf
         vpl = vpl if vpl is not None else self.vpl
@@ -200,6 +250,8 @@ class BandedGuiding:
             for tag, (ext, ts) in enumerate(self.halo_tensors(vpl)):
                 ops += halo_ops(ts, ext, self.rank, self.world, self.group, tag=1 + tag)
             reqs = post_exchange(ops)
+        if fallback:
+            self._miss.zero_()
         if split is None:
             split = overlap and bool(reqs)
         interior, edges = self.split_rows() if split else (None, [(self.r0, self.r1)])
@@ -209,6 +261,20 @@ class BandedGuiding:
             req.wait()
         for a, b in edges:
             self._launch(frame, a, b, cur_band, vpl, prev, g_in, g_out)
+        if fallback and self.has_prev:
+            if any_miss is None:
+                import torch
+                m = self._miss.clone().to(torch.int64)
+                if self.world > 1:
+                    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+                missed = int(m.item()) > 0
+            else:
+                missed = bool(any_miss(int(self._miss.item())))
+            if missed:
+                own = self.history_own()
+                full = gather(own) if gather is not None else gather_rows(own, self.rank, self.world, self.H,
+                                                                           self.group)
+                self._full_history_rerun(frame, cur_band, vpl, g_out, full)
         self.cur = 1 - self.cur
         self.has_prev = True
         self.prev_gb = cur

@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2112_09728_b200.bands import Extent, band_rows, check_band_geometry, halo_exchange
+from paper_2112_09728_b200.bands import Extent, band_rows, check_band_geometry, gather_rows, halo_exchange
 
 
 def test_band_rows_partition():
@@ -72,6 +72,36 @@ def test_halo_exchange_gloo(world, H, halo):
     out = ctx.Array("i", [0] * world)
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, H, 24, halo, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert list(out) == [1] * world
+
+
+def _gather_worker(rank, world, port, H, W, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(11)
+        full_a = torch.rand(H, W, 4, generator=g)
+        full_b = (torch.rand(H, W, generator=g) * 255).to(torch.uint8)
+        r0, r1 = band_rows(H, world, rank)
+        a, b = gather_rows([full_a[r0:r1].clone(), full_b[r0:r1].clone()], rank, world, H)
+        out[rank] = 1 if (torch.equal(a, full_a) and torch.equal(b, full_b)) else 0
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,H", [(2, 31), (3, 50)])
+def test_gather_rows_gloo(world, H):
+    """The full-history fallback's all-gather of unequal row bands."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Array("i", [0] * world)
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, H, 20, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
