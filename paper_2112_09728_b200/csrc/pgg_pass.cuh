@@ -389,7 +389,8 @@ struct EmSetup {
   V3<float> wol;     // view in the local frame
   float alb_r, alb_g, alb_b;  // luminance-weighted albedo (0.2126 r, 0.7152 g, 0.0722 b)
   float a2, kappa, g1o;  // g1o = G1(cos_o) / (4 cos_o)
-  float mx, my, il11, l21, il22, gnorm, pi;  // il11, il22 x c and l21 / c, c = sqrt(log2(e) / 2)
+  float mx, my, il11, l21, il22;  // il11, il22 x c and l21 / c, c = sqrt(log2(e) / 2)
+  float pg, qpi;                    // pi x (Gaussian normaliser), 1 - pi
   int flags;         // bit0 train this pixel, bit1 glossy, bit2 cos_o > 0
   int nb;            // neighbour budget N (mixture.py:324-328)
   uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
@@ -537,9 +538,8 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
   dir_to_sq_f(dl, o.qx, o.qy);
   const float z1 = (o.qx - S.mx) * S.il11;
   const float z2 = ((o.qy - S.my) - S.l21 * z1) * S.il22;
-  const float g = f_exp2(-(z1 * z1 + z2 * z2)) * S.gnorm;
-  const float num = S.pi * g;
-  const float den = num + (1.0f - S.pi) * bp;
+  const float num = S.pg * f_exp2(-(z1 * z1 + z2 * z2));
+  const float den = num + S.qpi * bp;
   o.r = num * f_rcp(fmaxf(den, 1e-30f));  // den = 0 only with num = 0 -> r = 0
   return true;
 }
@@ -586,9 +586,8 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   dir_to_sq_f(dl, qx, qy);
   const float z1 = (qx - S.mx) * S.il11;
   const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
-  const float g = f_exp2(-(z1 * z1 + z2 * z2)) * S.gnorm;
-  const float num = S.pi * g;
-  const float den = num + (1.0f - S.pi) * bp;
+  const float num = S.pg * f_exp2(-(z1 * z1 + z2 * z2));
+  const float den = num + S.qpi * bp;
   const float r = num * f_rcp(fmaxf(den, 1e-30f));
   const float wv = ok ? w : 0.0f;
   const float wr = ok ? w * r : 0.0f;
@@ -700,8 +699,8 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.il11 = (float)((double)L.il11 * GAUSS_C);
   S.l21 = (float)((double)L.l21 / GAUSS_C);
   S.il22 = (float)((double)L.il22 * GAUSS_C);
-  S.gnorm = L.gnorm;
-  S.pi = L.pi;
+  S.pg = L.pi * L.gnorm;
+  S.qpi = 1.0f - L.pi;
   S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
   S.nb = neighbor_budget(k, kmax);
 #ifdef PGG_PROF_NO_EM
