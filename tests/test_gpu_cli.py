@@ -95,3 +95,15 @@ def test_cli_commands(cuda_dev, tmp_path):
     assert cli.main(["render", "--frames", "0", "--out", out]) == 2
     img = metrics.read_pfm(os.path.join(out, "frame_0000.pfm"))
     assert img.shape == (32, 40, 3) and np.isfinite(img).all()
+
+
+@pytest.mark.parametrize("scene", ["indirect-corridor", "cornell-occluder"])
+def test_guiding_lowers_relmse(cuda_dev, scene):
+    """SPEC acceptance (pg/cli.py:240-272 run_ab): after a warm-up the guided
+    1-spp renders have lower relMSE against a converged reference than plain
+    path tracing, on the scenes built for indirect lighting."""
+    from paper_2112_09728_b200 import cli
+    from paper_2112_09728_b200 import scene as S
+    cfg = cli.RunConfig(width=64, height=64, warmup=64, pairs=16, ref_spp=1024)
+    res = cli.run_ab(S.load_scene(scene), cfg)
+    assert res["pg_over_pt"] < 0.97, res["pg_over_pt"]
