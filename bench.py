@@ -426,9 +426,9 @@ def bench_ours(args, rank, world, local_rank):
         e2e = bench_e2e(args, frames, cfg, dev, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        px, secs, thr = run_cpu_reference(rows_per_thread=160, threads=1)
+        px, secs, thr = run_cpu_reference(rows_per_thread=216, threads=1)
         cpu = {"value": px / secs / 1e6, "unit": "Mpixels/s", "cores": thr, "kind": "port",
-               "sample": f"one 1920x160 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
+               "sample": f"one 1920x216 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
                          f"sampling + training_pass, oracle port of pgtrace on 1 core",
                "stage_seconds": getattr(run_cpu_reference, "last_stages", None), **cpu_host()}
     if rank == 0:
