@@ -289,6 +289,13 @@ int pgg_primary_rays(const pgg_camera* cam, int32_t width, int32_t height, int64
 int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* points, double* px,
                 double* py, uint8_t* in_front, void* stream);
 
+/* sgmap.py:21-115 as float64 lane operations: op 0 square_to_disk (n x 2 ->
+ * n x 2), 1 disk_to_square (2 -> 2), 2 square_to_hemisphere (2 -> 3),
+ * 3 hemisphere_to_square (3 -> 2; the caller rejects z < -1e-9 first),
+ * 4 build_tangent_frame (n x 3 -> n x (t, b) 6), 5 to_world and 6 to_local
+ * (n x (t, b, n, v) 12 -> n x 3). */
+int pgg_sgmap(int32_t op, int64_t n, const double* in, double* out, void* stream);
+
 /* Image error (metrics.mse / metrics.rel_mse, metrics.py:24-38) of n
  * float32 elements: mean of (a - ref)^2, or of (a - ref)^2 / (ref^2 + 0.01)
  * when relative != 0, accumulated in float64 with a fixed reduction order

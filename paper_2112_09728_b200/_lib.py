@@ -109,6 +109,7 @@ _SIGS = {
     "pgg_sample_emitter": [ctypes.POINTER(Scene), c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_brdf": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_primary_rays": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p],
+    "pgg_sgmap": [c_i32, c_i64, c_p, c_p, c_p],
     "pgg_project": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p],
 }
 

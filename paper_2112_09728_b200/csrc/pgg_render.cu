@@ -750,6 +750,81 @@ __global__ void k_lane_project(pgg_camera cam, int w, int h, int64_t n, const do
   in_front[i] = fr ? 1 : 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// Equal-area square <-> hemisphere map and tangent frames as lane kernels
+// (sgmap.py:21-115), float64: op 0 square->disk (2 -> 2), 1 disk->square
+// (2 -> 2), 2 square->hemisphere (2 -> 3), 3 hemisphere->square (3 -> 2),
+// 4 tangent frame of a normal (3 -> t 3, b 3), 5 local->world and 6
+// world->local (t, b, n, v: 12 -> 3).
+
+__device__ void conc_disk(double px, double py, double& x, double& y) {
+  const double a = 2.0 * px - 1.0, b = 2.0 * py - 1.0;
+  double r = b, phi;
+  if (fabs(a) > fabs(b)) {
+    r = a;
+    phi = (0.25 * PI_D) * (b / a);
+  } else if (b != 0.0) {
+    phi = 0.5 * PI_D - (0.25 * PI_D) * (a / b);
+  } else {
+    phi = 0.0;  // the centre
+  }
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  x = r * cp;
+  y = r * sp;
+}
+
+__device__ void conc_square(double x, double y, double& u, double& v) {
+  const double rho = hypot(x, y);
+  double a = 0.0, b = 0.0;
+  if (rho != 0.0) {
+    if (fabs(x) >= fabs(y)) {
+      a = copysign(rho, x);
+      b = atan(y / x) * (4.0 / PI_D) * a;
+    } else {
+      b = copysign(rho, y);
+      a = atan(x / y) * (4.0 / PI_D) * b;
+    }
+  }
+  u = fmin(fmax((a + 1.0) * 0.5, 0.0), 1.0);
+  v = fmin(fmax((b + 1.0) * 0.5, 0.0), 1.0);
+}
+
+__global__ void k_lane_sgmap(int op, int64_t n, const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  switch (op) {
+    case 0: conc_disk(in[2 * i], in[2 * i + 1], out[2 * i], out[2 * i + 1]); break;
+    case 1: conc_square(in[2 * i], in[2 * i + 1], out[2 * i], out[2 * i + 1]); break;
+    case 2: {
+      double x, y;
+      conc_disk(in[2 * i], in[2 * i + 1], x, y);
+      const double r2 = x * x + y * y;  // Lambert lift (sgmap.py:59-65)
+      const double lift = sqrt(fmax(2.0 - r2, 0.0));
+      std3(out, i, d3(x * lift, y * lift, 1.0 - r2));
+      break;
+    }
+    case 3: {
+      const D3 w = ldd3(in, i);
+      const double s = sqrt(fmax(1.0 + w.z, 1e-30));
+      conc_square(w.x / s, w.y / s, out[2 * i], out[2 * i + 1]);
+      break;
+    }
+    case 4: {
+      const Onb f = onb(ldd3(in, i));
+      std3(out, 2 * i, f.t);
+      std3(out, 2 * i + 1, f.b);
+      break;
+    }
+    default: {
+      const Onb f{ldd3(in, 4 * i), ldd3(in, 4 * i + 1), ldd3(in, 4 * i + 2)};
+      const D3 v = ldd3(in, 4 * i + 3);
+      std3(out, i, op == 5 ? f.world(v) : f.local(v));
+    }
+  }
+}
+
 int table_doubles(const pgg_scene* s) {
   return s->n_mat * MAT_STRIDE + s->n_sph * SPH_STRIDE + s->n_quad * QUAD_STRIDE + s->n_emit;
 }
@@ -874,6 +949,13 @@ int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n,
   if (n == 0) return PGG_OK;
   k_lane_project<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, points,
                                                                                      px, py, in_front);
+  return pgg_rt::check_launch();
+}
+
+int pgg_sgmap(int32_t op, int64_t n, const double* in, double* out, void* stream) {
+  if (op < 0 || op > 6 || n < 0 || !in || !out) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  k_lane_sgmap<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(op, n, in, out);
   return pgg_rt::check_launch();
 }
 

@@ -184,3 +184,34 @@ def test_checkpoint_roundtrip(tmp_path, cuda_dev):
     np.testing.assert_array_equal(h.stats, g.stats)
     with pytest.raises(GB.CheckpointError):
         GB.checkpoint_load(p, expect_size=(9, 17))
+
+
+def test_sgmap_lane_kernels(cuda_dev, kat):
+    """sgmap (pgg_sgmap lane kernels) vs the oracle's float64 restatement and
+    the reference's round-trip KATs."""
+    import torch
+
+    from paper_2112_09728_b200 import sgmap
+    r = np.random.default_rng(12)
+    p = r.uniform(0, 1, (50000, 2))
+    p[:4] = [[0.5, 0.5], [0.0, 0.0], [1.0, 0.5], [0.5, 1.0]]
+    d = sgmap.square_to_hemisphere(p)
+    np.testing.assert_allclose(d, O.sq_to_dir(p), rtol=0, atol=1e-15)
+    v = d / np.linalg.norm(d, axis=-1, keepdims=True)
+    np.testing.assert_allclose(sgmap.hemisphere_to_square(v), O.dir_to_sq(v), rtol=0, atol=1e-14)
+    disk = sgmap.square_to_disk(p)
+    np.testing.assert_allclose(sgmap.disk_to_square(disk), p, rtol=0, atol=1e-14)
+    n = r.standard_normal((1000, 3))
+    n /= np.linalg.norm(n, axis=-1, keepdims=True)
+    t, b = sgmap.build_tangent_frame(n)
+    ot, ob = O.onb(n)
+    np.testing.assert_array_equal(t, ot)
+    np.testing.assert_array_equal(b, ob)
+    loc = r.standard_normal((1000, 3))
+    np.testing.assert_allclose(sgmap.to_world(t, b, n, loc), O.local_to_world(ot, ob, n, loc), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(sgmap.to_local(t, b, n, loc), O.world_to_local(ot, ob, n, loc), rtol=0, atol=1e-15)
+    assert sgmap.square_density_to_solid_angle(2 * np.pi) == 1.0
+    with pytest.raises(ValueError):
+        sgmap.hemisphere_to_square(np.array([[0.0, 0.0, -1.0]]))
+    tp = torch.as_tensor(p[:10], device=cuda_dev)
+    assert torch.is_tensor(sgmap.square_to_hemisphere(tp))
