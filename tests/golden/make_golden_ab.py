@@ -1,0 +1,36 @@
+"""Golden outputs of the reference's `ab` experiment (pg/cli.py:240-272),
+made by running the REFERENCE itself in the build container:
+
+    python tests/golden/make_golden_ab.py
+
+Small configuration (32x32, warm-up 24, 8 pairs, 256-spp reference) so the
+CPU run takes seconds; tests/test_gpu_cli.py compares the GPU CLI's run_ab
+on the same configuration.  Output: tests/golden/ab_small.json
+"""
+
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from pgtrace import cli  # noqa: E402
+from pgtrace import scene as sc  # noqa: E402
+
+CFG = dict(width=32, height=32, warmup=24, pairs=8, ref_spp=256, seed=3)
+
+
+def main():
+    os.environ["PG_THREADS"] = "4"
+    out = {"config": CFG}
+    for name in ("cornell-occluder", "indirect-corridor", "glossy-box"):
+        r = cli.run_ab(sc.load_scene(name), cli.RunConfig(**CFG))
+        out[name] = {k: float(r[k]) for k in ("pg_mean_relmse", "pt_mean_relmse", "pg_over_pt")}
+        print(name, out[name])
+    with open(os.path.join(HERE, "ab_small.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

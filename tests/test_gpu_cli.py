@@ -107,3 +107,20 @@ def test_guiding_lowers_relmse(cuda_dev, scene):
     cfg = cli.RunConfig(width=64, height=64, warmup=64, pairs=16, ref_spp=1024)
     res = cli.run_ab(S.load_scene(scene), cfg)
     assert res["pg_over_pt"] < 0.97, res["pg_over_pt"]
+
+
+@pytest.mark.parametrize("scene", ["cornell-occluder", "indirect-corridor", "glossy-box"])
+def test_ab_matches_reference_run(cuda_dev, scene):
+    """The reference's own ab experiment (tests/golden/ab_small.json, made by
+    tests/golden/make_golden_ab.py running pgtrace): plain path tracing to
+    1e-6 relative (float64 lanes), the guided arm -- 24 warm-up + 8 frames of
+    the full render/reproject/sample/EM loop -- to 1e-3."""
+    import json
+
+    from paper_2112_09728_b200 import cli
+    from paper_2112_09728_b200 import scene as S
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ab_small.json")))
+    res = cli.run_ab(S.load_scene(scene), cli.RunConfig(**gold["config"]))
+    ref = gold[scene]
+    assert res["pt_mean_relmse"] == pytest.approx(ref["pt_mean_relmse"], rel=1e-6)
+    assert res["pg_mean_relmse"] == pytest.approx(ref["pg_mean_relmse"], rel=1e-3)
