@@ -124,3 +124,18 @@ def test_ab_matches_reference_run(cuda_dev, scene):
     ref = gold[scene]
     assert res["pt_mean_relmse"] == pytest.approx(ref["pt_mean_relmse"], rel=1e-6)
     assert res["pg_mean_relmse"] == pytest.approx(ref["pg_mean_relmse"], rel=1e-3)
+
+
+def test_flicker_matches_reference_run(cuda_dev):
+    """Temporal MSE of a guided static-camera run vs the reference's own run
+    (tests/golden/ab_small.json['flicker'])."""
+    import json
+
+    from paper_2112_09728_b200 import cli, metrics
+    from paper_2112_09728_b200 import scene as S
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ab_small.json")))["flicker"]
+    c = gold["config"]
+    sess = cli.RenderSession(S.load_scene("cornell-occluder"), cli.RunConfig(**c))
+    frames = [sess.run_frame(f).image for f in range(c["warmup"] + c["frames"])][c["warmup"]:]
+    got = [r.value for r in metrics.flicker_series(frames)]
+    np.testing.assert_allclose(got, gold["temporal_mse"], rtol=2e-3)
