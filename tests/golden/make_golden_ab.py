@@ -28,6 +28,11 @@ def main():
         r = cli.run_ab(sc.load_scene(name), cli.RunConfig(**CFG))
         out[name] = {k: float(r[k]) for k in ("pg_mean_relmse", "pt_mean_relmse", "pg_over_pt")}
         print(name, out[name])
+    # SPEC criterion 7 setup (no warm-up): the reference's own ratio
+    ucfg = dict(width=64, height=64, warmup=0, pairs=16, ref_spp=1024, seed=4)
+    r = cli.run_ab(sc.load_scene("cornell-occluder"), cli.RunConfig(**ucfg))
+    out["untrained"] = {"config": ucfg, **{k: float(r[k]) for k in ("pg_mean_relmse", "pt_mean_relmse", "pg_over_pt")}}
+    print("untrained", out["untrained"])
     # flicker (pg/cli.py:208-233): static camera, guided warm-up, temporal MSE rows
     fcfg = dict(width=32, height=32, frames=4, warmup=8, mode="pg", seed=5)
     session = cli.RenderSession(sc.load_scene("cornell-occluder"), cli.RunConfig(**fcfg))
