@@ -915,7 +915,11 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
   L.l22 = (float)l22;
   L.il11 = 1.0f / L.l11;
   L.il22 = 1.0f / L.l22;
+#ifdef PGG_PROF_NO_TRUNC
+  L.z = 1.0f;  // measurement-only build
+#else
   L.z = trunc_mass_bvn(mx, my, sxx, syy, sxy, L.l11, L.l21, L.l22);
+#endif
   // 1 / (2 pi l11 l22 Z) / (2 pi)
   L.gnorm = L.il11 * L.il22 * (0.025330295910584444f / L.z);
   L.pi = pi;

@@ -172,7 +172,11 @@ PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const floa
   if (C.rotate_mean) {
     bool keep;
     float ox, oy;
+#ifdef PGG_PROF_NO_ROT
+    keep = true, ox = p0.x, oy = p0.y;  // measurement-only build
+#else
     rotate_or_reject(v3(ndp.x, ndp.y, ndp.z), v3(nd.x, nd.y, nd.z), p0.x, p0.y, keep, ox, oy);
+#endif
     if (!keep) return;
     p0.x = ox;
     p0.y = oy;
@@ -767,7 +771,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
 #else
   if (A.has_smp) {
 #endif
+#ifdef PGG_PROF_NO_GUIDE
+    const bool guided = false;  // measurement-only build
+#else
     const bool guided = (!glossy || (double)rough >= C.rough_min_guide) && g1.w >= 1.0f;
+#endif
     CholD cd;
     cd.mx = g0.x;
     cd.my = g0.y;
