@@ -471,16 +471,18 @@ def bench_frame_loop(dev, frames=16, warmup=4):
     for f in range(warmup):
         sess.run_frame(f)
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for f in range(warmup, warmup + frames):
+    per = []
+    for f in range(warmup, warmup + frames):  # per-frame events, median (robust to allocator / clock hiccups)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         r = sess.run_frame(f)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / frames
+        e1.record()
+        torch.cuda.synchronize(dev)
+        per.append(e0.elapsed_time(e1))
+    ms = statistics.median(per)
     return {"scene": "cornell-occluder (panning)", "ms_per_frame": ms, "Mpixels/s": W * H / (ms * 1e-3) / 1e6,
-            "mean_path_length": r.mean_path_length, "frames": frames,
-            "kernels": "k_gbuffer, k_guiding_pass (reproject+sample), k_render, k_guiding_pass (EM)"}
+            "ms_per_frame_min_max": [min(per), max(per)], "mean_path_length": r.mean_path_length,
+            "frames": frames, "kernels": "k_gbuffer, k_guiding_pass (reproject+sample), k_render, k_guiding_pass (EM)"}
 
 
 def bench_e2e(args, frames, cfg, dev, world):
