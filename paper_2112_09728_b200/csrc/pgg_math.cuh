@@ -844,6 +844,9 @@ PGG_HD float glb_w(int i) {
 // reference's piecewise 24-point rule (mixture.py:84-126) up to that rule's
 // own quadrature error (<= 2.5e-5 relative on extreme lobes, ~1e-15
 // typically); |r| >= 0.999 falls back to the reference rule itself.
+#ifndef PGG_BVN_FAST
+#define PGG_BVN_FAST 1
+#endif
 PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double sxy, float l11, float l21,
                             float l22) {
   // standardised bounds and correlation in float32 (the result is float32;
@@ -858,8 +861,16 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
   } else {
     const float a1 = (0.0f - mxf) * isx, b1 = (1.0f - mxf) * isx;
     const float a2 = (0.0f - myf) * isy, b2 = (1.0f - myf) * isy;
-    z = ndtr_diff(b1, a1) * ndtr_diff(b2, a2);
+    const float pa = ndtr_diff(b1, a1), pb = ndtr_diff(b2, a2);
+    z = pa * pb;
+    // Frechet bounds: |P(A and B) - P(A) P(B)| <= min(1 - P(A), 1 - P(B)); when
+    // one marginal leaves less than 1e-6 z outside [0,1] the correlation term
+    // is below 1e-6 relative (the reference rule itself is good to 8e-6)
+#if PGG_BVN_FAST
+    if (sxy != 0.0 && fminf(1.0f - pa, 1.0f - pb) > 1e-6f * z) {
+#else
     if (sxy != 0.0) {
+#endif
       const float asr = asinf(r);
       const float hk0 = a1 * a2, hs0 = 0.5f * (a1 * a1 + a2 * a2);
       const float hk1 = b1 * a2, hs1 = 0.5f * (b1 * b1 + a2 * a2);
