@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-frame-loop", action="store_true")
+    ap.add_argument("--bands", action="store_true", help="row-band path even at N=1 (exercises the NCCL code)")
     return ap.parse_args()
 
 
@@ -350,8 +351,8 @@ def bench_bands(args, rank, world, local_rank):
                 "config": {"workload": WORKLOADS[args.workload][3] + ", row bands + NCCL halo exchange",
                            "parallelism": f"bands{world}"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                             "note": "per GPU, step time incl. halo exchange"},
+                             "frac": achieved / peak, "traffic": ncu_traffic(args.workload) if world == 1 else None,
+                             "peak_kind": peak_kind, "note": "per GPU, step time incl. halo exchange"},
                 "clocks": clk.summary(), "gpu_launches": args.steps, "e2e": None, "cpu_baseline": None,
                 "halo_misses": band.halo_misses()}
         print(json.dumps(line), flush=True)
@@ -588,15 +589,16 @@ def main():
         return
     import torch
     import torch.distributed as dist
-    if world > 1:
+    use_dist = world > 1 or args.bands
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
     __graft_entry__.build()
-    if world > 1 and args.workload != "1080p":
+    if args.bands or (world > 1 and args.workload != "1080p"):
         bench_bands(args, rank, world, local_rank)
     else:
         bench_ours(args, rank, world, local_rank)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 
