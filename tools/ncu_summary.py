@@ -39,8 +39,11 @@ def ncu(*args):
     return subprocess.run(["ncu", *args], capture_output=True, text=True).stdout
 
 
+KFILTER = []  # optional ["-k", "regex:<name>"] for multi-kernel reports
+
+
 def raw_metrics(rep):
-    raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+    raw = list(csv.reader(io.StringIO(ncu("-i", rep, *KFILTER, "--page", "raw", "--csv"))))
     hdr, vals = raw[0], raw[2] if len(raw) > 2 else raw[1]
     units = raw[1] if len(raw) > 2 else [""] * len(hdr)
     return dict(zip(hdr, vals)), dict(zip(hdr, units))
@@ -80,7 +83,8 @@ def main(rep):
     print("\n## warp stall samples")
     for k, v in sorted(stalls.items(), key=lambda kv: -float(kv[1]))[:10]:
         print(f"  {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):28s} {100 * float(v) / tot:5.1f}%")
-    src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"))))
+    src = list(csv.reader(io.StringIO(ncu("-i", rep, *KFILTER, "--page", "source", "--csv", "--print-source",
+                                          "cuda,sass"))))
     cur = hdr2 = None
     agg = []
     for r in src:
@@ -103,6 +107,10 @@ def main(rep):
 
 
 if __name__ == "__main__":
+    if "--kernel" in sys.argv:
+        i = sys.argv.index("--kernel")
+        KFILTER = ["-k", "regex:" + sys.argv[i + 1]]
+        del sys.argv[i:i + 2]
     if len(sys.argv) > 3 and sys.argv[2] == "--traffic":
         write_traffic(sys.argv[1], sys.argv[3])
     else:
