@@ -125,6 +125,10 @@ __device__ __forceinline__ bool in_unit(double n, double e) {
   return n > -1e-280 && tiny_negative_quotient_nonneg(n, e);
 }
 
+__device__ __forceinline__ int table_doubles_d(const pgg_scene& sc) {
+  return sc.n_mat * MAT_STRIDE + sc.n_sph * SPH_STRIDE + sc.n_quad * QUAD_STRIDE + sc.n_emit;
+}
+
 struct Hit {
   bool hit, front;
   double t;
@@ -410,22 +414,40 @@ struct LaneResult {
   int segs;
 };
 
+// Lane accumulators (L, Li, T, Tr, vy: 15 doubles) parked in shared memory:
+// they change once per bounce, and keeping them out of the register file
+// leaves the intersection loops their registers.
+struct Park {
+  volatile double* p;  // field k of this thread at p[k * stride]
+  int stride;
+  __device__ D3 get(int k) const { return d3(p[(3 * k) * stride], p[(3 * k + 1) * stride], p[(3 * k + 2) * stride]); }
+  __device__ void set(int k, D3 v) const {
+    p[(3 * k) * stride] = v.x;
+    p[(3 * k + 1) * stride] = v.y;
+    p[(3 * k + 2) * stride] = v.z;
+  }
+};
+enum { P_L = 0, P_LI = 1, P_T = 2, P_TR = 3, P_VY = 4, P_FIELDS = 5 };
+
 __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool valid0, bool front0, D3 pos, D3 nrm,
-                                 int mat, D3 wo, uint64_t& st, int64_t lane_own) {
+                                 int mat, D3 wo, uint64_t& st, int64_t lane_own, const Park& pk) {
   const pgg_render_config& C = A.cfg;
   LaneResult R;
-  R.L = d3(0, 0, 0);
-  R.Li = d3(0, 0, 0);
-  R.vy = d3(0, 0, 0);
   R.vv = false;
   R.vs = 0;
   R.segs = 0;
+  const D3 zero = d3(0, 0, 0);
+  pk.set(P_LI, zero);
+  pk.set(P_VY, zero);
   if (!valid0) {
     R.L = S.bg;
+    R.Li = zero;
+    R.vy = zero;
     return R;
   }
-  if (front0) R.L = R.L + S.emission(mat);
-  D3 T = d3(1, 1, 1), Tr = d3(0, 0, 0);
+  pk.set(P_L, front0 ? zero + S.emission(mat) : zero);
+  pk.set(P_T, d3(1, 1, 1));
+  pk.set(P_TR, zero);
   const bool do_nee = C.nee && S.ne > 0;
   for (int depth = 0; depth < C.max_depth; ++depth) {
     const int kd = S.kind(mat);
@@ -442,8 +464,8 @@ __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool vali
       if (lpdf > 0.0 && cx > 0.0 && any_pos(f)) {
         if (!cast<true>(S, pos, ld, RAY_EPS, dist - RAY_EPS).hit) c = le * f * (cx / lpdf);
       }
-      R.L = R.L + T * c;
-      if (depth >= 1) R.Li = R.Li + Tr * c;
+      pk.set(P_L, pk.get(P_L) + pk.get(P_T) * c);
+      if (depth >= 1) pk.set(P_LI, pk.get(P_LI) + pk.get(P_TR) * c);
     }
     D3 wi;
     double pdf;
@@ -467,14 +489,14 @@ __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool vali
     ok = ok && pdf > 0.0 && ci > 0.0;
     if (!ok) break;
     const D3 w = f * (ci / pdf);
-    T = T * w;
-    if (depth >= 1) Tr = Tr * w;
+    pk.set(P_T, pk.get(P_T) * w);
+    if (depth >= 1) pk.set(P_TR, pk.get(P_TR) * w);
     if (depth == 0) R.vs = strat;
     const Hit h = cast<false>(S, pos, wi, RAY_EPS, INFINITY);
     ++R.segs;
     if (!h.hit) {
-      R.L = R.L + T * S.bg;
-      if (depth >= 1) R.Li = R.Li + Tr * S.bg;
+      pk.set(P_L, pk.get(P_L) + pk.get(P_T) * S.bg);
+      if (depth >= 1) pk.set(P_LI, pk.get(P_LI) + pk.get(P_TR) * S.bg);
       break;
     }
     pos = h.pos;
@@ -483,11 +505,14 @@ __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool vali
     wo = neg(wi);
     if (depth == 0) {
       R.vv = true;
-      R.vy = h.pos;
-      Tr = d3(1, 1, 1);
-      if (h.front) R.Li = R.Li + S.emission(h.mat);
+      pk.set(P_VY, h.pos);
+      pk.set(P_TR, d3(1, 1, 1));
+      if (h.front) pk.set(P_LI, pk.get(P_LI) + S.emission(h.mat));
     }
   }
+  R.L = pk.get(P_L);
+  R.Li = pk.get(P_LI);
+  R.vy = pk.get(P_VY);
   return R;
 }
 
@@ -496,7 +521,7 @@ __device__ LaneResult trace_lane(const RenderArgs& A, const SceneS& S, bool vali
 #endif
 constexpr int RT_W = 32, RT_H = 4;  // pixel tile of one 128-thread block
 
-__device__ void render_pixel(const RenderArgs& A, const SceneS& S, int x, int yl, int& segs, int& bad) {
+__device__ void render_pixel(const RenderArgs& A, const SceneS& S, int x, int yl, int& segs, int& bad, const Park& pk) {
   const pgg_render_config& C = A.cfg;
   const int y = C.row0 + yl;
   const int64_t own = (int64_t)yl * C.width + x;
@@ -515,7 +540,7 @@ __device__ void render_pixel(const RenderArgs& A, const SceneS& S, int x, int yl
     const int64_t lane = own * C.spp + s;
     uint64_t st = A.out.states ? A.out.states[lane] : pcg_lane(C.key, pix * (uint64_t)C.spp + (uint64_t)s);
     R = trace_lane(A, S, valid, front, d3(pr.x, pr.y, pr.z), d3(nd.x, nd.y, nd.z), m, d3(va.x, va.y, va.z), st,
-                   own * C.spp + s);
+                   own * C.spp + s, pk);
     if (A.out.states) A.out.states[lane] = st;
     segs += R.segs;
     if (!finite3(R.L)) {
@@ -558,7 +583,9 @@ __global__ void __launch_bounds__(RT_W * RT_H, PGG_RENDER_MIN_BLOCKS) k_render(c
   int segs = 0, bad = 0;
   const int x = blockIdx.x * RT_W + threadIdx.x;
   const int yl = blockIdx.y * RT_H + threadIdx.y;
-  if (x < C.width && yl < C.rows) render_pixel(A, S, x, yl, segs, bad);
+  const int tid = threadIdx.x + RT_W * threadIdx.y;
+  const Park pk{smem + table_doubles_d(A.scene) + tid, RT_W * RT_H};
+  if (x < C.width && yl < C.rows) render_pixel(A, S, x, yl, segs, bad, pk);
   if (A.out.counters) {
     const unsigned sg = __reduce_add_sync(0xffffffffu, (unsigned)segs);
     const unsigned bd = __reduce_add_sync(0xffffffffu, (unsigned)bad);
@@ -886,7 +913,8 @@ int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const 
   A.s_tag = depth0 ? depth0->tag : nullptr;
   A.out = *out;
   const dim3 grd((cfg->width + RT_W - 1) / RT_W, (cfg->rows + RT_H - 1) / RT_H);
-  k_render<<<grd, dim3(RT_W, RT_H), table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(A);
+  const size_t smem = (table_doubles(scene) + 3 * P_FIELDS * RT_W * RT_H) * sizeof(double);
+  k_render<<<grd, dim3(RT_W, RT_H), smem, reinterpret_cast<cudaStream_t>(stream)>>>(A);
   return pgg_rt::check_launch();
 }
 
