@@ -467,10 +467,23 @@ PGG_HD float om_u01(uint32_t u, float) { return (float)(0x100000000ULL - (uint64
 PGG_HD double om_u01(uint32_t u, double) { return 1.0 - u01d(u); }  // exact in float64
 
 // Lambert cosine sample (scene.py:311-316); z = sqrt(1 - u1)
+// Lambert azimuth: no decision depends on it, so the device uses MUFU
+// sin/cos on the folded angle (direction error < 1e-6)
+PGG_HD void sincos_turn_lambert(uint32_t u, float* s, float* c) {
+#if defined(__CUDA_ARCH__) && PGG_SMP_MUFU_TRIG
+  const float th = (float)(int32_t)u * 1.4629180792671596e-09f;  // 2 pi u - (u >= 1/2 ? 2 pi : 0)
+  *s = __sinf(th);
+  *c = __cosf(th);
+#else
+  sincos_turn(u, s, c);
+#endif
+}
+PGG_HD void sincos_turn_lambert(uint32_t u, double* s, double* c) { sincos_turn(u, s, c); }
+
 template <class T> PGG_HD V3<T> sample_cosine(uint32_t a, uint32_t b) {
   const T r = m_sqrt(u01(a, T()));
   T s, c;
-  sincos_turn(b, &s, &c);
+  sincos_turn_lambert(b, &s, &c);
   return {r * c, r * s, m_sqrt(m_max(om_u01(a, T()), T(0)))};
 }
 
