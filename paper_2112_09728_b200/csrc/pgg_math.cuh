@@ -186,6 +186,21 @@ PGG_HD double m_clamp01(double x) { return fmin(fmax(x, 0.0), 1.0); }
 PGG_HD bool m_isfinite(float x) { return isfinite(x); }
 PGG_HD bool m_isfinite(double x) { return isfinite(x); }
 
+// square roots on the sampler's float paths (Lambert lift, Box-Muller
+// radius): MUFU-based on the device when PGG_SMP_SQRT_FAST (~1e-7 relative,
+// inside the acceptance guard band and the direction tolerance)
+#ifndef PGG_SMP_SQRT_FAST
+#define PGG_SMP_SQRT_FAST 1
+#endif
+PGG_HD float smp_sqrt(float x) {
+#if defined(__CUDA_ARCH__) && PGG_SMP_SQRT_FAST
+  return f_sqrt(x);
+#else
+  return m_sqrt(x);
+#endif
+}
+PGG_HD double smp_sqrt(double x) { return m_sqrt(x); }
+
 // sin/cos of pi*x (exact argument scaling on the device)
 #ifndef PGG_SMP_MUFU_TRIG
 #define PGG_SMP_MUFU_TRIG 1  // concentric-map sin/cos on MUFU (abs error < 2^-20.5): 0.5387 -> 0.5364 ms
@@ -365,7 +380,7 @@ template <class T> PGG_HD V3<T> sq_to_dir(T px, T py) {
   T s, c;
   m_sincospi(q, &s, &c);
   const T r2 = r * r;
-  const T lift = m_sqrt(m_max(T(2) - r2, T(0)));
+  const T lift = smp_sqrt(m_max(T(2) - r2, T(0)));
   return {r * c * lift, r * s * lift, T(1) - r2};
 }
 
@@ -591,7 +606,7 @@ PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
   } else {
     lnu = m_log1p(-(float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f);
   }
-  const float r = m_sqrt(-2.0f * lnu);
+  const float r = smp_sqrt(-2.0f * lnu);
   float s, c;
   sincos_turn(b, &s, &c);
   z0 = r * c;
