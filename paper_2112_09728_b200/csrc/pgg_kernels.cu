@@ -49,6 +49,9 @@ constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this ra
 #ifndef PGG_TILE_S
 #define PGG_TILE_S 1
 #endif
+#ifndef PGG_OPAQUE_Y
+#define PGG_OPAQUE_Y 1
+#endif
 #ifndef PGG_STASH
 #define PGG_STASH 1
 #endif
@@ -156,7 +159,14 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   if (kTile) mbar_wait(bar, 0);
   if (!active) return;
   float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#if PGG_OPAQUE_Y
+  // through a shuffle, opaque to the register allocator: under pressure the
+  // row is then kept or spilled (one reload) instead of being rebuilt from
+  // tid / ctaid / kernel parameters in every slot of the record loop
+  const int y = __shfl_sync(__activemask(), A.cfg.row0 + yl, lane);
+#else
   const int y = A.cfg.row0 + yl;
+#endif
 #if PGG_STASH
   // park Gamma in shared memory: 8 registers fewer live across the EM loop
   float4* stash = reinterpret_cast<float4*>(s_em);
