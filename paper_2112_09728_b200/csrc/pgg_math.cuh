@@ -986,7 +986,9 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
   const double half = rmul(0.5, radd(sxx, syy));
   const double dd = rsub(sxx, syy);
   const double q = radd(rmul(0.25, rmul(dd, dd)), rmul(sxy, sxy));
-  const double delta = sqrt(fmax(q, 0.0));
+  // zero operands (reset and fresh lobes: sxy = 0) would take the slow
+  // paths of the float64 sqrt / division; the results are the same values
+  const double delta = q > 0.0 ? sqrt(q) : 0.0;
   const bool reset = rsub(half, delta) < 1e-6;
   if (reset) {
     sxx = 0.05;
@@ -994,7 +996,7 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
     sxy = 0.0;
   }
   const double l11 = sqrt(sxx);
-  const double l21 = sxy / l11;
+  const double l21 = sxy == 0.0 ? sxy : sxy / l11;
   const double l22 = sqrt(fmax(rsub(syy, rmul(l21, l21)), 1e-30));
   LobeF L;
   L.mx = mxf;
@@ -1027,7 +1029,9 @@ PGG_HD float gauss_sr(const LobeF& L, float sx, float sy) {
 // (mixture.py:324-328), computed in float64 like the reference
 PGG_HD int neighbor_budget(float k, int kmax) {
   const double kk = fmin((double)k, (double)kmax);
-  const double raw = radd(rmul(rsub(1.0, kk / (double)kmax), 15.0), 5.0);
+  // kk / kmax; a power-of-two kmax (64 by default) divides exactly as a product
+  const double q = (kmax & (kmax - 1)) == 0 ? kk * (1.0 / (double)kmax) : kk / (double)kmax;
+  const double raw = radd(rmul(rsub(1.0, q), 15.0), 5.0);
   return (int)floor(radd(raw, 0.5));
 }
 

@@ -732,7 +732,7 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.my = L.my;
   // exponent -(z1^2 + z2^2)/2 evaluated as exp2(-(z1'^2 + z2'^2)) with z' = c z
   S.il11 = (float)((double)L.il11 * GAUSS_C);
-  S.l21 = (float)((double)L.l21 / GAUSS_C);
+  S.l21 = (float)((double)L.l21 * (1.0 / GAUSS_C));  // constant reciprocal: no float64 division
   S.il22 = (float)((double)L.il22 * GAUSS_C);
   S.pg = L.pi * L.gnorm;
   S.qpi = 1.0f - L.pi;
