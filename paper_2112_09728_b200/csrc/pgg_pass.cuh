@@ -698,7 +698,7 @@ PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, i
   const float sw = acc[0], swr = acc[1];
   if (!(sw > 0.0f)) return;  // no information: unchanged, k unchanged
   const double k = g1.w;
-  const double eta = fmax(1.0 / (k + 1.0), 1.0 / (double)kmax);
+  const double eta = 1.0 / fmin(k + 1.0, (double)kmax);  // = max(1/(k+1), 1/kMax): division is monotone
   const double om1 = 1.0 - eta;
   const double ed = eta / fmax((double)swr, 1e-8);
   o0.x = (float)(om1 * g0.x + ed * (double)acc[2]);
