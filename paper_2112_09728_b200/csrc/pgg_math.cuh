@@ -107,6 +107,16 @@ PGG_HD float r_div(float a, float b) {
 }
 
 // sqrt via rsqrt (~2 ulp), 0 -> 0
+// sqrt.approx (one MUFU.SQRT; relative error ~2^-22) for non-negative x
+PGG_HD float f_sqrt_mufu(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return sqrtf(x);
+#endif
+}
 PGG_HD float f_sqrt(float x) {
 #ifdef __CUDA_ARCH__
   return x > 0.0f ? x * rsqrtf(x) : 0.0f;

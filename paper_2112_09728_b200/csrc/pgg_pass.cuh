@@ -376,16 +376,28 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
 // re-evaluated in float64.  The band (4e-6 (R + 1)) bounds the float32
 // error of r cos / r sin: on the device sin/cos come from MUFU.SIN/COS on
 // [-pi, pi) (abs error < 2^-20.5, x R) and rint from the 1.5 * 2^23 add.
+#ifndef PGG_LOOP_TRIM
+#define PGG_LOOP_TRIM 1
+#endif
 PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
-  const float r = (float)radius * f_sqrt(u01f(ua));
   const float band = 4e-6f * ((float)radius + 1.0f);
 #if defined(__CUDA_ARCH__) && PGG_EM_FAST
+#if PGG_LOOP_TRIM
+  const float r = (float)radius * f_sqrt_mufu(u01f(ua));
+#else
+  const float r = (float)radius * f_sqrt(u01f(ua));
+#endif
   const float th = (float)(int32_t)ub * 1.4629180792671596e-09f;  // 2 pi u - (u >= 1/2 ? 2 pi : 0)
   const float fx = r * __cosf(th), fy = r * __sinf(th);
   const float kM = 12582912.0f;  // 1.5 * 2^23: x + kM rounds x to the nearest integer (even on ties)
   const float tx = fx + kM, ty = fy + kM;
   const float rx = fx - (tx - kM), ry = fy - (ty - kM);
+#if PGG_LOOP_TRIM
+  const float hb = 0.5f - band;  // loop invariant: one compare on |r| per coordinate
+  if (fabsf(rx) > hb || fabsf(ry) > hb) {
+#else
   if (0.5f - fabsf(rx) < band || 0.5f - fabsf(ry) < band) {
+#endif
     const Off2 o = disk_offset_d(ua, ub, radius);
     dx = o.x;
     dy = o.y;
@@ -394,6 +406,7 @@ PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& d
   dx = __float_as_int(tx) - 0x4B400000;
   dy = __float_as_int(ty) - 0x4B400000;
 #else
+  const float r = (float)radius * f_sqrt(u01f(ua));
   float s, c;
   sincos_turn(ub, &s, &c);
   const float fx = r * c, fy = r * s;
@@ -621,11 +634,21 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   dir_to_sq_f(dl, qx, qy);
   const float z1 = (qx - S.mx) * S.il11;
   const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+#if PGG_LOOP_TRIM
+  // -(z1^2 + z2^2) with the negation folded into the products (same value);
+  // r is finite, so the masked w r is 0 * r = 0 as before
+  const float num = S.pg * f_exp2(fmaf(-z1, z1, -(z2 * z2)));
+  const float den = num + S.qpi * bp;
+  const float r = num * f_rcp(fmaxf(den, 1e-30f));
+  const float wv = ok ? w : 0.0f;
+  const float wr = wv * r;
+#else
   const float num = S.pg * f_exp2(-(z1 * z1 + z2 * z2));
   const float den = num + S.qpi * bp;
   const float r = num * f_rcp(fmaxf(den, 1e-30f));
   const float wv = ok ? w : 0.0f;
   const float wr = ok ? w * r : 0.0f;
+#endif
   // qx, qy are finite even for masked records (dir_to_sq_f clamps, NaN -> 0)
   acc[0] += wv;
   acc[1] += wr;
