@@ -112,7 +112,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // Measured alternatives (2/4/8 lanes per pixel with a butterfly reduction,
 // a split stage-1 / EM kernel pair) were slower; see DESIGN.md section 4.
 
-template <bool kTile>
+template <bool kTile, bool kFull>
 __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
     k_guiding_pass(const PassArgs A, const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmL,
                    int R) {
@@ -180,10 +180,10 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
 #else
       const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
 #endif
-      em_partial(A, V, S, x, y, c_jmul, c_jadd, acc);
+      em_partial<kFull>(A, V, S, x, y, c_jmul, c_jadd, acc);
     } else {
       const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
-      em_partial(A, V, S, x, y, c_jmul, c_jadd, acc);
+      em_partial<kFull>(A, V, S, x, y, c_jmul, c_jadd, acc);
     }
   }
   const int64_t own = (int64_t)yl * A.cfg.width + x;
@@ -229,18 +229,26 @@ bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool kTile>
-int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
+template <bool kTile, bool kFull>
+int launch_pass_t(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
   const SmemLayout SL(R, kTile);
   static bool attr_set = false;  // opt in once to the largest layout this instantiation can use
   if (!attr_set) {
     const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);
-    cudaFuncSetAttribute(k_guiding_pass<kTile>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
+    cudaFuncSetAttribute(k_guiding_pass<kTile, kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
     attr_set = true;
   }
   const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
-  k_guiding_pass<kTile><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
+  k_guiding_pass<kTile, kFull><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
   return check_launch();
+}
+
+// whole-frame VPL planes (no row band) take the instantiation without the
+// per-candidate halo checks
+template <bool kTile>
+int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
+  if (A.vpl.row0 == 0 && A.vpl.rows == A.cfg.height) return launch_pass_t<kTile, true>(A, my, ml, R, st);
+  return launch_pass_t<kTile, false>(A, my, ml, R, st);
 }
 
 // ---------------------------------------------------------------------------

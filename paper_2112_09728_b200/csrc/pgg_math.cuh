@@ -452,9 +452,10 @@ PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float rho2 = x * x + y * y;
 #if defined(__CUDA_ARCH__) && PGG_SQ_RAW
-  const float rho = rho2 > 0.0f ? rho2 * rsqrtf(rho2) : 0.0f;
+  // floors instead of guards: a zero rho2 / max gives 0 * finite = 0
+  const float rho = rho2 * rsqrtf(fmaxf(rho2, 1e-36f));
   const float mx = fmaxf(ax, ay);
-  const float t = mx > 0.0f ? fminf(ax, ay) * f_rcp(mx) : 0.0f;
+  const float t = fminf(ax, ay) * f_rcp(fmaxf(mx, 1e-36f));
 #else
   const float rho = rho2 > 0.0f ? rho2 * r_rsqrt(rho2) : 0.0f;
   const float mx = fmaxf(ax, ay);
@@ -468,8 +469,14 @@ PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
   const bool xdom = ax >= ay;
   const float a = copysignf(xdom ? rho : u, x);
   const float b = copysignf(xdom ? u : rho, y);
+#ifdef __CUDA_ARCH__
+  // (a + 1) / 2 as one fma: halving commutes with rounding, same value
+  sx = __saturatef(fmaf(a, 0.5f, 0.5f));
+  sy = __saturatef(fmaf(b, 0.5f, 0.5f));
+#else
   sx = fminf(fmaxf((a + 1.0f) * 0.5f, 0.0f), 1.0f);
   sy = fminf(fmaxf((b + 1.0f) * 0.5f, 0.0f), 1.0f);
+#endif
 }
 
 // ---------------------------------------------------------------------------

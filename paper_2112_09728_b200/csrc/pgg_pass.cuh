@@ -668,7 +668,9 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, i
 // pixel's own VPL; slot s >= 1 draws u1 = draw s-1 and u2 = draw 18+s of
 // the pixel's stream (the reference draws all 19 u1 then all 19 u2,
 // guide_buffers.py:144-145) and rounds the disk offset.
-template <class VS>
+// kFull: the VPL planes cover the whole frame (every launch but a row band's),
+// so no candidate can miss them and no halo misses are counted.
+template <bool kFull = false, class VS>
 PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, const uint64_t* jmul,
                        const uint64_t* jadd, float* acc) {
   const pgg_config& C = A.cfg;
@@ -676,7 +678,7 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   const int vr0 = A.vpl.row0;
   const unsigned vrows = (unsigned)A.vpl.rows;
   if (S.nb <= 0) return;
-  if ((unsigned)(y - vr0) >= vrows) {  // own row outside the VPL rows: every slot misses
+  if (!kFull && (unsigned)(y - vr0) >= vrows) {  // own row outside the VPL rows: every slot misses
     count_miss(A.halo_misses);
     return;
   }
@@ -703,15 +705,15 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     disk_offset(ua, ub, C.radius, dx, dy);
     const int cx = x + dx, cy = y + dy;
     const bool in_frame = (unsigned)cx < W && (unsigned)cy < H;
-    const bool in_vpl = (unsigned)(cy - vr0) < vrows;
-    misses += (in_frame && !in_vpl) ? 1 : 0;
+    const bool in_vpl = kFull || (unsigned)(cy - vr0) < vrows;
+    if (!kFull) misses += (in_frame && !in_vpl) ? 1 : 0;
     bool ok = in_frame && in_vpl;
     const auto idx = ok ? base + (decltype(base))dy * stride + dx : base;
     const float4 vy = V.y_at(idx);
     ok = ok && vy.w != 0.0f;  // VPL invalid or not BRDF-strategy
     em_accumulate(S, vy, V, idx, ok, acc, n_raw);
   }
-  if (misses) count_miss(A.halo_misses, misses);
+  if (!kFull && misses) count_miss(A.halo_misses, misses);
 }
 
 // Online M-step (mixture.py:276-321) in float64 from the float32 sums.
