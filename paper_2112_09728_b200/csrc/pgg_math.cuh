@@ -967,10 +967,13 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
     if (sxy != 0.0) {
 #endif
       const float asr = asinf(r);
-      const float hk0 = a1 * a2, hs0 = 0.5f * (a1 * a1 + a2 * a2);
-      const float hk1 = b1 * a2, hs1 = 0.5f * (b1 * b1 + a2 * a2);
-      const float hk2 = a1 * b2, hs2 = 0.5f * (a1 * a1 + b2 * b2);
-      const float hk3 = b1 * b2, hs3 = 0.5f * (b1 * b1 + b2 * b2);
+      // corner terms pre-scaled by log2(e): exp(x) = ex2(x log2 e), one
+      // multiply fewer per exponential in the node loop
+      constexpr float L2E = 1.4426950408889634f;
+      const float hk0 = L2E * (a1 * a2), hs0 = (0.5f * L2E) * (a1 * a1 + a2 * a2);
+      const float hk1 = L2E * (b1 * a2), hs1 = (0.5f * L2E) * (b1 * b1 + a2 * a2);
+      const float hk2 = L2E * (a1 * b2), hs2 = (0.5f * L2E) * (a1 * a1 + b2 * b2);
+      const float hk3 = L2E * (b1 * b2), hs3 = (0.5f * L2E) * (b1 * b1 + b2 * b2);
       // node count per |r| for float32 accuracy (measured); one
       // loop over a constant table keeps the code small (icache)
       const int cls = ar < 0.3f ? 0 : ar < 0.75f ? 1 : ar < 0.925f ? 2 : ar < 0.96f ? 3 : ar < 0.99f ? 4 : 5;
@@ -981,8 +984,8 @@ PGG_HD float trunc_mass_bvn(double mx, double my, double sxx, double syy, double
       for (int i = off; i < off + cnt; ++i) {
         const float sn = f_sin(asr * glb_u(i));
         const float inv = f_rcp(1.0f - sn * sn);
-        const float e = f_exp((sn * hk0 - hs0) * inv) - f_exp((sn * hk1 - hs1) * inv) -
-                        f_exp((sn * hk2 - hs2) * inv) + f_exp((sn * hk3 - hs3) * inv);
+        const float e = f_exp2((sn * hk0 - hs0) * inv) - f_exp2((sn * hk1 - hs1) * inv) -
+                        f_exp2((sn * hk2 - hs2) * inv) + f_exp2((sn * hk3 - hs3) * inv);
         acc = fmaf(glb_w(i), e, acc);
       }
       z += acc * asr * 0.079577471545947667884f;  // 1/(4 pi)
