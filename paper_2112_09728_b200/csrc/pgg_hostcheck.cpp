@@ -21,6 +21,7 @@ int pgghc_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_
   PassArgs A;
   memset(&A, 0, sizeof(A));
   A.cfg = *cfg;
+  pass_args_finish(A);
   A.cur = *cur;
   if (prev) A.prev = *prev;
   A.gin = *gamma_prev;
@@ -110,6 +111,7 @@ extern "C" int pgghc_train_records(const pgg_config* cfg, const pgg_gbuffer* cur
   PassArgs A;
   memset(&A, 0, sizeof(A));
   A.cfg = *cfg;
+  pass_args_finish(A);
   A.cur = *cur;
   A.gin = *gamma;
   A.vpl = *vpl;

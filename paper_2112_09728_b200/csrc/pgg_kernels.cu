@@ -502,6 +502,7 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   PassArgs A;
   memset(&A, 0, sizeof(A));
   A.cfg = *cfg;
+  pass_args_finish(A);
   A.cur = *cur;
   if (prev) A.prev = *prev;
   A.gin = *gamma_prev;
@@ -553,6 +554,7 @@ int pgg_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_g
   PassArgs A;
   memset(&A, 0, sizeof(A));
   A.cfg = *cfg;
+  pass_args_finish(A);
   A.cur = *cur;
   A.gin = *gamma;
   A.vpl = *vpl;

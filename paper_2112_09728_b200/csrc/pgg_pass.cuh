@@ -37,7 +37,18 @@ struct PassArgs {
   pgg_samples smp;
   int has_prev, has_vpl, has_grep, has_smp;
   int32_t* halo_misses;
+  // record-loop constants precomputed on the host (kernel parameters, so the
+  // loop reads them as constant-bank operands instead of holding registers)
+  float em_radius16;  // (float) cfg.radius * 2^-16 (exact): R sqrt(u 2^-32) = em_radius16 sqrt(u)
+  float em_hband;     // 0.5 - the candidate-offset rounding guard band
 };
+
+// fills the derived PassArgs fields from cfg (every construction site)
+inline void pass_args_finish(PassArgs& A) {
+  const float rf = (float)A.cfg.radius;
+  A.em_radius16 = rf * 1.52587890625e-05f;
+  A.em_hband = 0.5f - 4e-6f * (rf + 1.0f);
+}
 
 PGG_HD float4 f4(float x, float y, float z, float w) {
   float4 v;
@@ -379,13 +390,22 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
 #ifndef PGG_LOOP_TRIM
 #define PGG_LOOP_TRIM 1
 #endif
+PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy);
 PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
-  const float band = 4e-6f * ((float)radius + 1.0f);
+  const float rf = (float)radius;
+  disk_offset_k(ua, ub, radius, rf * 1.52587890625e-05f, 0.5f - 4e-6f * (rf + 1.0f), dx, dy);
+}
+// rf16 = (float)radius * 2^-16, hb = 0.5 - 4e-6 ((float)radius + 1)
+PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy) {
+  const float band = 0.5f - hb;
+  const float rf = rf16 * 65536.0f;
 #if defined(__CUDA_ARCH__) && PGG_EM_FAST
 #if PGG_LOOP_TRIM
-  const float r = (float)radius * f_sqrt_mufu(u01f(ua));
+  // sqrt(u 2^-32) = sqrt(u) 2^-16 exactly: the scale joins the radius
+  (void)rf;
+  const float r = rf16 * f_sqrt_mufu((float)ua);
 #else
-  const float r = (float)radius * f_sqrt(u01f(ua));
+  const float r = rf * f_sqrt(u01f(ua));
 #endif
   const float th = (float)(int32_t)ub * 1.4629180792671596e-09f;  // 2 pi u - (u >= 1/2 ? 2 pi : 0)
   const float fx = r * __cosf(th), fy = r * __sinf(th);
@@ -393,8 +413,7 @@ PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& d
   const float tx = fx + kM, ty = fy + kM;
   const float rx = fx - (tx - kM), ry = fy - (ty - kM);
 #if PGG_LOOP_TRIM
-  const float hb = 0.5f - band;  // loop invariant: one compare on |r| per coordinate
-  if (fabsf(rx) > hb || fabsf(ry) > hb) {
+  if (fabsf(rx) > hb || fabsf(ry) > hb) {  // one compare on |r| per coordinate
 #else
   if (0.5f - fabsf(rx) < band || 0.5f - fabsf(ry) < band) {
 #endif
@@ -406,7 +425,8 @@ PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& d
   dx = __float_as_int(tx) - 0x4B400000;
   dy = __float_as_int(ty) - 0x4B400000;
 #else
-  const float r = (float)radius * f_sqrt(u01f(ua));
+  (void)band;
+  const float r = rf * f_sqrt(u01f(ua));
   float s, c;
   sincos_turn(ub, &s, &c);
   const float fx = r * c, fy = r * s;
@@ -702,7 +722,7 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     sa = sa * PCG_MUL + PCG_INC;
     sb = sb * PCG_MUL + PCG_INC;
     int dx, dy;
-    disk_offset(ua, ub, C.radius, dx, dy);
+    disk_offset_k(ua, ub, C.radius, A.em_radius16, A.em_hband, dx, dy);
     const int cx = x + dx, cy = y + dy;
     const bool in_frame = (unsigned)cx < W && (unsigned)cy < H;
     const bool in_vpl = kFull || (unsigned)(cy - vr0) < vrows;
