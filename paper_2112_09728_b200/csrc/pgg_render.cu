@@ -129,6 +129,10 @@ __device__ __forceinline__ int table_doubles_d(const pgg_scene& sc) {
   return sc.n_mat * MAT_STRIDE + sc.n_sph * SPH_STRIDE + sc.n_quad * QUAD_STRIDE + sc.n_emit;
 }
 
+#ifndef PGG_QUAD_PREREJECT
+#define PGG_QUAD_PREREJECT 1
+#endif
+
 struct Hit {
   bool hit, front;
   double t;
@@ -172,6 +176,15 @@ __device__ Hit cast(const SceneS& S, D3 o, D3 d, double t_min, double t_max) {
       // t = num / den > t_min > 0 needs num and den of one sign: the other
       // half of the planes is rejected without the division
       if (!(num > 0.0 ? den > 0.0 : (num < 0.0 && den < 0.0))) continue;
+#if PGG_QUAD_PREREJECT
+      // planes certainly beyond min(best, t_max) skip the division: with
+      // |num| > bound |den| (1 + 2^-50) the exact quotient exceeds bound by
+      // more than the product's rounding, so RN(num / den) >= bound
+      {
+        const double bound = fmin(best, t_max);
+        if (fabs(num) > __dmul_rn(__dmul_rn(bound, fabs(den)), 1.0 + 0x1p-50)) continue;
+      }
+#endif
       const double t = num / den;
       if (!(t > t_min && t < t_max && t < best)) continue;
       const D3 rel = (o + d * t) - corner;
