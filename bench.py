@@ -281,7 +281,9 @@ def bench_reference(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / args.steps, "ms_per_1080p_frame": 1e3 * W * H / (mpix * 1e6),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "1920x1080 1spp guiding pass (reproject+sample/pdf+EM), CPU oracle port of pgtrace",
+            "config": {"workload": "1920x1080 1 spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM "
+                                   "per frame (BASELINE configs[1]); N>1 = N independent streams",
+                       "implementation": "CPU oracle port of pgtrace (reproject, depth-0 sampling, training_pass)",
                        "sample": sample},
             "cpu_baseline": {"value": mpix, "unit": "Mpixels/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": mpix, "unit": "Mpixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
