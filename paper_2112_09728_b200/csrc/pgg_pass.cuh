@@ -387,6 +387,9 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
 // re-evaluated in float64.  The band (4e-6 (R + 1)) bounds the float32
 // error of r cos / r sin: on the device sin/cos come from MUFU.SIN/COS on
 // [-pi, pi) (abs error < 2^-20.5, x R) and rint from the 1.5 * 2^23 add.
+#ifndef PGG_TILE_OOB
+#define PGG_TILE_OOB 1
+#endif
 #ifndef PGG_LOOP_TRIM
 #define PGG_LOOP_TRIM 1
 #endif
@@ -500,6 +503,7 @@ PGG_COLD bool record_valid_d(float yx, float yy, float yz, V3<float> x, V3<float
 // VPL accessors for the record loop: straight from global memory (L2), or
 // from a shared-memory tile (own 32 x 8 block + EM halo) staged by TMA.
 struct VplGlobal {
+  static constexpr bool kZeroOOB = false;  // no padding: out-of-frame candidates must be tested
   const float* y;
   const float* L;
   int width, row0;
@@ -511,6 +515,7 @@ struct VplGlobal {
   PGG_MHD float4 L_at(int64_t i) const { return ld4(L, i); }
 };
 struct VplTile {
+  static constexpr bool kZeroOOB = true;  // TMA zero-fills tile elements outside the frame
   const float4* y;  // shared memory, [rows][cols]
   const float4* L;
   int x0, y0, cols;  // frame coordinates of tile element (0, 0)
@@ -526,6 +531,7 @@ struct VplTile {
 // base register instead of two generic pointers, L at a fixed offset.
 // Device-only (the host build reads VplGlobal).
 struct VplTileS {
+  static constexpr bool kZeroOOB = true;  // TMA zero-fills tile elements outside the frame
   uint32_t y;      // shared address of tile element (0, 0) of the y plane
   uint32_t off_l;  // byte offset of the L plane
   int x0, y0, cols;
@@ -724,11 +730,15 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     int dx, dy;
     disk_offset_k(ua, ub, C.radius, A.em_radius16, A.em_hband, dx, dy);
     const int cx = x + dx, cy = y + dy;
-    const bool in_frame = (unsigned)cx < W && (unsigned)cy < H;
+    // whole-frame VPLs staged by TMA: every candidate (|d| <= R) lies in the
+    // tile and those outside the frame read TMA's zero fill, i.e. an invalid
+    // VPL (w = 0) -- the reference's "out of frame -> unused" without a test
+    constexpr bool kNoBounds = PGG_TILE_OOB && kFull && VS::kZeroOOB;
+    const bool in_frame = kNoBounds || ((unsigned)cx < W && (unsigned)cy < H);
     const bool in_vpl = kFull || (unsigned)(cy - vr0) < vrows;
     if (!kFull) misses += (in_frame && !in_vpl) ? 1 : 0;
     bool ok = in_frame && in_vpl;
-    const auto idx = ok ? base + (decltype(base))dy * stride + dx : base;
+    const auto idx = (kNoBounds || ok) ? base + (decltype(base))dy * stride + dx : base;
     const float4 vy = V.y_at(idx);
     ok = ok && vy.w != 0.0f;  // VPL invalid or not BRDF-strategy
     em_accumulate(S, vy, V, idx, ok, acc, n_raw);
