@@ -131,8 +131,19 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
 
+    def wait_ready(self, timeout=5.0):
+        """block until nvidia-smi has produced its first sample (its start-up
+        takes longer than a short timed region)"""
+        end = time.monotonic() + timeout
+        while self.proc and not self.rows and time.monotonic() < end:
+            time.sleep(0.01)
+
     def mark(self, t0, t1):
         self.window = (t0, t1)
+        # one sample after the region closes it on both sides
+        end = time.monotonic() + 0.5
+        while self.proc and not any(t >= t1 for t, _ in self.rows) and time.monotonic() < end:
+            time.sleep(0.005)
 
     def __exit__(self, *a):
         if self.proc:
@@ -148,6 +159,9 @@ class ClockSampler:
             # samples inside the timed region (+ one 20 ms sampling period either side)
             t0, t1 = self.window
             inside = [r for t, r in self.rows if t0 - 0.025 <= t <= t1 + 0.025]
+            if not inside and self.rows:  # region shorter than the sampling period: nearest samples
+                near = sorted(self.rows, key=lambda tr: min(abs(tr[0] - t0), abs(tr[0] - t1)))
+                inside = [r for _, r in near[:2]]
             rows = inside or rows[-3:]
         sm = [float(r[0]) for r in rows if r and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
@@ -332,6 +346,7 @@ def bench_bands(args, rank, world, local_rank):
     dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
+        clk.wait_ready()
         h0 = time.monotonic()
         t0.record(stream)
         for _ in range(args.steps):
@@ -389,7 +404,7 @@ def bench_ours(args, rank, world, local_rank):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
-        time.sleep(0.1)
+        clk.wait_ready()
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize(dev)
