@@ -4,6 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17
 //        -shared -Xcompiler -fPIC -I include csrc/pgg_kernels.cu -o libpgg.so
 #include <cuda.h>
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -243,11 +244,15 @@ int launch_pass_t(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& m
   return check_launch();
 }
 
-// whole-frame VPL planes (no row band) take the instantiation without the
-// per-candidate halo checks
+// VPL planes that cover every candidate row of the launch (the whole frame,
+// or a row band with its full ceil(radius) halo) take the instantiation
+// without the per-candidate halo checks: no candidate can miss them
 template <bool kTile>
 int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
-  if (A.vpl.row0 == 0 && A.vpl.rows == A.cfg.height) return launch_pass_t<kTile, true>(A, my, ml, R, st);
+  const int halo = (int)ceil(A.cfg.radius > 0.0 ? A.cfg.radius : 0.0);
+  const int lo = std::max(0, A.cfg.row0 - halo);
+  const int hi = std::min(A.cfg.height, A.cfg.row0 + A.cfg.rows + halo);
+  if (A.vpl.row0 <= lo && A.vpl.row0 + A.vpl.rows >= hi) return launch_pass_t<kTile, true>(A, my, ml, R, st);
   return launch_pass_t<kTile, false>(A, my, ml, R, st);
 }
 
