@@ -261,14 +261,17 @@ def run_cpu_reference(rows_per_thread=32, threads=None, frame=5, seed=0):
         t0 = time.perf_counter()
         g = O.reproject(st[r0:r1], gp_, gc_)           # guide_buffers.reproject
         t1 = time.perf_counter()
-        O.sample_frame(g, gc_, seed, frame)              # lobe_from_stats + _sample_first_bounce
+        smp = O.sample_frame(g, gc_, seed, frame)        # lobe_from_stats + _sample_first_bounce
         t2 = time.perf_counter()
-        O.train(g, vc_, gc_, seed=seed, frame=frame)     # training_pass
+        tr = O.train(g, vc_, gc_, seed=seed, frame=frame)  # training_pass
         t3 = time.perf_counter()
         if threads == 1:
             stages["reproject"] += t1 - t0
             stages["sample"] += t2 - t1
             stages["train"] += t3 - t2
+            # inputs and outputs of the timed sample, for the in-bench parity check
+            run_cpu_reference.last_io = dict(gp=gp, gc=gc, vc=vc, gamma_in=st, frame=frame, seed=seed,
+                                             gamma_reproj=g, samples=smp, gamma_trained=tr)
 
     t = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
@@ -276,6 +279,50 @@ def run_cpu_reference(rows_per_thread=32, threads=None, frame=5, seed=0):
     if threads == 1:
         run_cpu_reference.last_stages = {k: round(v, 3) for k, v in stages.items()}
     return W * h, time.perf_counter() - t, threads
+
+
+def parity_vs_cpu(dev):
+    """Run the GPU pass on the exact input the cpu_baseline leg just timed
+    (a 1920x216 frame: reproject + 1 spp depth-0 sampling + EM, random k in
+    [0, 16)) and compare with the oracle's outputs: SURVEY 8a single-kernel
+    policy figures (Gamma per-channel relative error with a 1e-7 floor, k,
+    strategy/validity tags, directions, pdfs)."""
+    import numpy as np
+    import torch
+
+    from paper_2112_09728_b200.layout import GammaPlanes, GBufferPlanes, PassConfig, VplPlanes
+    from paper_2112_09728_b200.session import run_pass
+    io = getattr(run_cpu_reference, "last_io", None)
+    if io is None:
+        return None
+    cur = GBufferPlanes.from_ref(io["gc"], device=dev)
+    prev = GBufferPlanes.from_ref(io["gp"], device=dev)
+    r = run_pass(PassConfig(seed=io["seed"], spp=1), io["frame"], cur, GammaPlanes.from_aos(io["gamma_in"], dev),
+                 prev=prev, vpl=VplPlanes.from_ref(io["vc"], device=dev), want_reproj=True)
+    torch.cuda.synchronize(dev)
+
+    def rel(a, b):
+        return np.abs(a.astype(np.float64) - b) / np.maximum(np.abs(b.astype(np.float64)), 1e-7)
+
+    got, ref = r.gamma.to_aos().cpu().numpy(), io["gamma_trained"]
+    rep = rel(r.gamma_reproj.to_aos().cpu().numpy(), io["gamma_reproj"])
+    g = rel(got, ref)
+    n = got.shape[0] * got.shape[1]
+    d = r.samples.dir.cpu().numpy().reshape(n, 4)
+    t = r.samples.tag.cpu().numpy().reshape(n)
+    smp = io["samples"]
+    ok = smp["valid"][:, 0] & ((t >> 1) & 1).astype(bool)
+    pr = rel(d[ok, 3], smp["pdf"][ok, 0])
+    return {"sample": f"the cpu_baseline input ({got.shape[1]}x{got.shape[0]}, random k in [0, 16))",
+            "gamma_rel_p9999": float(np.percentile(g, 99.99)), "gamma_rel_max": float(g.max()),
+            "gamma_reproj_rel_max": float(rep.max()),
+            "k_equal": bool(np.array_equal(got[..., 7], ref[..., 7])),
+            "tags_equal": bool(np.array_equal(t & 1, smp["strategy"][:, 0]) and
+                               np.array_equal(((t >> 1) & 1).astype(bool), smp["valid"][:, 0])),
+            "dir_abs_max": float(np.abs(d[:, :3] - smp["wi"][:, 0]).max()),
+            "pdf_rel_p9999": float(np.percentile(pr, 99.99)) if pr.size else 0.0,
+            "policy": "SURVEY 8a: gamma p99.99 <= 1e-4, max <= 1e-3, k exact; tags exact; dirs <= 1e-5; "
+                      "pdf p99.99 <= 1e-4"}
 
 
 def bench_reference(args, rank, world):
@@ -449,6 +496,7 @@ def bench_ours(args, rank, world, local_rank):
                "sample": f"one 1920x216 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
                          f"sampling + training_pass, oracle port of pgtrace on 1 core",
                "stage_seconds": getattr(run_cpu_reference, "last_stages", None), **cpu_host()}
+        cpu["parity"] = parity_vs_cpu(dev)
     if rank == 0:
         metric = ("guiding-pass Mpixels/s at 1080p" if args.workload == "1080p"
                   else f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)")

@@ -309,6 +309,28 @@ const char* pgg_status_string(int status);
 const char* pgg_last_cuda_error(void);
 int pgg_abi_version(void);
 
+/* Diagnostics (test-only; not on the product path).  Each runs the device
+ * functions of pgg_guiding_pass over a whole frame / batch and records the
+ * discrete decisions the reference makes, so tests can compare them with the
+ * reference's float64 arithmetic at frame scale:
+ *   pgg_debug_em_offsets  the 19 candidate offsets (dx, dy) of every pixel,
+ *       int8 [width*height][19][2], as training_pass draws them
+ *       (guide_buffers.py:140-161: rint of 10 sqrt(u1) cos/sin(2 pi u2));
+ *       *rechecks += number of offsets re-decided in float64 (guard band)
+ *   pgg_debug_bm_accept   Box-Muller proposal acceptance p in [0,1]^2
+ *       (mixture.py:216-230) for n proposals, lobe i / per_lobe from float32
+ *       Gamma stats[8]; draws (u1, u2) as u32 pairs; out bit0 accepted, bit1
+ *       re-decided in float64
+ *   pgg_debug_reproject   reprojection decision per pixel of cfg's band
+ *       (guide_buffers.py:78-137): bit0 accepted, bit1 gates re-decided in
+ *       float64, bit2 rejected by the mean rotation (z < 0), bit3 rejected by
+ *       the depth / normal gates */
+int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream);
+int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
+                        int32_t* rechecks, void* stream);
+int pgg_debug_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                        const pgg_gamma_in* gamma_prev, uint8_t* decisions, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -423,12 +423,15 @@ def m_step(stats, sq, w, r, ok, kmax=KMAX):
 # ---------------------------------------------------------------------------
 # reprojection (pg/guide_buffers.py:78-137)
 
-def reproject(stats_prev, prev, cur, depth_rel_tol=0.1, normal_dot_min=0.9, rotate_mean=True):
+def reproject(stats_prev, prev, cur, depth_rel_tol=0.1, normal_dot_min=0.9, rotate_mean=True, return_parts=False):
     """Nearest-neighbour history fetch along motion vectors.
 
     stats_prev: (H,W,8) float32.  prev/cur: G-buffer namespaces (valid,
     depth, normal, pos, motion, has_history, cam_origin).  Returns (H,W,8)
-    float32."""
+    float32; with ``return_parts`` also a namespace of the per-pixel
+    decisions (flat): ``source_ok`` (valid, history, in frame, source valid),
+    ``gates_ok`` (+ depth and normal gates), ``accepted`` (+ mean rotation
+    z >= 0)."""
     h, w = stats_prev.shape[:2]
     src_stats = stats_prev.reshape(-1, 8).astype(np.float64)
     out = fresh_stats(h * w)
@@ -438,12 +441,14 @@ def reproject(stats_prev, prev, cur, depth_rel_tol=0.1, normal_dot_min=0.9, rota
     ok = cur.valid & cur.has_history & (tx >= 0) & (tx < w) & (ty >= 0) & (ty < h)
     src = (np.clip(ty, 0, h - 1) * w + np.clip(tx, 0, w - 1)).reshape(-1)
     ok = ok.reshape(-1) & prev.valid.reshape(-1)[src]
+    ok_src = ok.copy()
     d_exp = np.linalg.norm(cur.pos.reshape(-1, 3) - prev.cam_origin, axis=-1)
     d_prev = prev.depth.reshape(-1)[src]
     ok &= np.abs(d_prev - d_exp) < depth_rel_tol * np.maximum(d_exp, 1e-12)
     n_prev = prev.normal.reshape(-1, 3)[src]
     n_cur = cur.normal.reshape(-1, 3)
     ok &= dot3(n_prev, n_cur) > normal_dot_min
+    ok_gates = ok.copy()
     sel = np.nonzero(ok)[0]
     if sel.size:
         got = src_stats[src[sel]]
@@ -458,40 +463,51 @@ def reproject(stats_prev, prev, cur, depth_rel_tol=0.1, normal_dot_min=0.9, rota
             got[:, (MEAN_X, MEAN_Y)] = dir_to_sq(d_c)
             sel, got = sel[keep], got[keep]
         out[sel] = got
-    return out.reshape(h, w, 8).astype(np.float32)
+    out = out.reshape(h, w, 8).astype(np.float32)
+    if return_parts:
+        acc = np.zeros(h * w, dtype=bool)
+        acc[sel] = True
+        return out, SimpleNamespace(source_ok=ok_src, gates_ok=ok_gates, accepted=acc)
+    return out
 
 
 # ---------------------------------------------------------------------------
 # training pass (pg/guide_buffers.py:140-231, 262-283)
 
-def candidates(h, w, radius, state):
+def candidates(h, w, radius, state, pix=None):
     """Self + 19 uniform-disk neighbours; 38 draws per pixel, u1 block then
-    u2 block (pg/guide_buffers.py:140-161).  Returns (cand, used)."""
-    p = h * w
+    u2 block (pg/guide_buffers.py:140-161).  Returns (cand, used).
+
+    ``pix``: flat frame indices of the pixels whose candidates are drawn
+    (default: every pixel); ``state`` holds their streams in that order.
+    Candidates are frame indices either way."""
+    pix = np.arange(h * w) if pix is None else np.asarray(pix, dtype=np.int64)
     u1 = np.stack([draw_unit(state) for _ in range(SLOTS - 1)], axis=1)
     u2 = np.stack([draw_unit(state) for _ in range(SLOTS - 1)], axis=1)
     rr = radius * np.sqrt(u1)
     ang = 2.0 * np.pi * u2
-    cx = (np.arange(p) % w)[:, None] + np.rint(rr * np.cos(ang)).astype(np.int64)
-    cy = (np.arange(p) // w)[:, None] + np.rint(rr * np.sin(ang)).astype(np.int64)
+    cx = (pix % w)[:, None] + np.rint(rr * np.cos(ang)).astype(np.int64)
+    cy = (pix // w)[:, None] + np.rint(rr * np.sin(ang)).astype(np.int64)
     inside = (cx >= 0) & (cx < w) & (cy >= 0) & (cy < h)
-    cand = np.concatenate([np.arange(p)[:, None], np.clip(cy, 0, h - 1) * w + np.clip(cx, 0, w - 1)], axis=1)
-    used = np.concatenate([np.ones((p, 1), dtype=bool), inside], axis=1)
+    cand = np.concatenate([pix[:, None], np.clip(cy, 0, h - 1) * w + np.clip(cx, 0, w - 1)], axis=1)
+    used = np.concatenate([np.ones((pix.size, 1), dtype=bool), inside], axis=1)
     return cand, used
 
 
-def records(stats, lb, vpl, gbuf, cand, used):
+def records(stats, lb, vpl, gbuf, cand, used, pix=None):
     """Per (pixel, slot) record: square point, luminance weight, E-step
-    responsibility and validity (pg/guide_buffers.py:170-231)."""
+    responsibility and validity (pg/guide_buffers.py:170-231).  ``pix``:
+    frame indices of the receivers (rows of stats / lb / cand), default all."""
     p, c = cand.shape
-    x = gbuf.pos.reshape(-1, 3)
-    n = gbuf.normal.reshape(-1, 3)
-    wo = gbuf.view.reshape(-1, 3)
-    kind = np.broadcast_to(gbuf.kind.reshape(-1)[:, None], (p, c))
-    rough = np.broadcast_to(gbuf.roughness.reshape(-1)[:, None], (p, c))
-    alb = np.broadcast_to(gbuf.albedo.reshape(-1, 3)[:, None, :], (p, c, 3))
+    own = slice(None) if pix is None else np.asarray(pix, dtype=np.int64)
+    x = gbuf.pos.reshape(-1, 3)[own]
+    n = gbuf.normal.reshape(-1, 3)[own]
+    wo = gbuf.view.reshape(-1, 3)[own]
+    kind = np.broadcast_to(gbuf.kind.reshape(-1)[own][:, None], (p, c))
+    rough = np.broadcast_to(gbuf.roughness.reshape(-1)[own][:, None], (p, c))
+    alb = np.broadcast_to(gbuf.albedo.reshape(-1, 3)[own][:, None, :], (p, c, 3))
     ok = used & vpl.valid.reshape(-1)[cand] & (vpl.strategy.reshape(-1)[cand] == STRAT_BRDF)
-    ok &= gbuf.valid.reshape(-1)[:, None]
+    ok &= gbuf.valid.reshape(-1)[own][:, None]
     d = vpl.y.reshape(-1, 3)[cand] - x[:, None, :]
     dist = np.linalg.norm(d, axis=-1)
     ok &= dist > 1e-9
@@ -514,20 +530,28 @@ def records(stats, lb, vpl, gbuf, cand, used):
     return sq, wgt, r, ok
 
 
-def train(stats_f32, vpl, gbuf, kmax=KMAX, seed=0, frame=0, radius=RADIUS, return_parts=False):
+def train(stats_f32, vpl, gbuf, kmax=KMAX, seed=0, frame=0, radius=RADIUS, return_parts=False, rows=None):
     """One EM epoch per valid pixel over the screen-space VPL neighbourhood
-    (pg/guide_buffers.py:262-283).  Returns (H,W,8) float32."""
+    (pg/guide_buffers.py:262-283).  Returns (H,W,8) float32.
+
+    ``rows=(r0, r1)`` trains only frame rows r0..r1-1 (returns those rows),
+    with the whole frame as context: global pixel indices key the streams
+    and the in-frame test uses the full height, so the band equals the same
+    rows of the whole-frame result (the reference's per-pixel independence,
+    pg/guide_buffers.py:274)."""
     h, w = stats_f32.shape[:2]
-    st = stats_f32.reshape(-1, 8).astype(np.float64)
+    r0, r1 = (0, h) if rows is None else rows
+    pix = np.arange(r0 * w, r1 * w, dtype=np.int64)
+    st = stats_f32.reshape(-1, 8)[pix].astype(np.float64)
     lb = lobe(st)
-    state = seed_lanes(seed, frame, np.arange(h * w), stream=1)
-    cand, used = candidates(h, w, radius, state)
+    state = seed_lanes(seed, frame, pix, stream=1)
+    cand, used = candidates(h, w, radius, state, pix)
     used &= np.arange(SLOTS)[None, :] < budget(st[:, EPOCH], kmax)[:, None]
-    sq, wgt, r, ok = records(st, lb, vpl, gbuf, cand, used)
+    sq, wgt, r, ok = records(st, lb, vpl, gbuf, cand, used, pix)
     new = m_step(st, sq, wgt, r, ok, kmax)
-    keep = ~gbuf.valid.reshape(-1)
+    keep = ~gbuf.valid.reshape(-1)[pix]
     new[keep] = st[keep]
-    out = new.reshape(h, w, 8).astype(np.float32)
+    out = new.reshape(r1 - r0, w, 8).astype(np.float32)
     if return_parts:
         return out, SimpleNamespace(cand=cand, used=used, sq=sq, w=wgt, r=r, ok=ok, lobe=lb)
     return out
@@ -612,7 +636,7 @@ def first_bounce(pos, nrm, kind, rough, wo, stats, lb, guided, state):
     return wi, pdf, strat, valid
 
 
-def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROUGH_MIN_GUIDE, lb=None):
+def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROUGH_MIN_GUIDE, lb=None, rows=None):
     """Depth-0 sampling of every valid pixel x spp lane, as the render pass
     issues it (pg/ptrace.py:449-475, 254-291): lane key pix*spp+s,
     ``nee_draws`` draws consumed by next-event estimation first, guided iff
@@ -620,28 +644,34 @@ def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROU
 
     Returns dict with wi (P,spp,3), pdf (P,spp), strategy (P,spp) uint8,
     valid (P,spp) bool, draws (P,spp) = PCG32 draws the sampler consumed
-    after the NEE draws; invalid pixels are all zero."""
+    after the NEE draws; invalid pixels are all zero.
+
+    ``rows=(r0, r1)``: only frame rows r0..r1-1 (P = (r1-r0) W, lane keys
+    stay global)."""
     h, w = stats_f32.shape[:2]
-    p = h * w
-    st = stats_f32.reshape(-1, 8).astype(np.float64)
+    r0, r1 = (0, h) if rows is None else rows
+    band = slice(r0 * w, r1 * w)
+    p = (r1 - r0) * w
+    st = stats_f32.reshape(-1, 8)[band].astype(np.float64)
     if lb is None:
         lb = lobe(st)
-    valid = gbuf.valid.reshape(-1)
-    kind = gbuf.kind.reshape(-1)
-    rough = gbuf.roughness.reshape(-1)
+    valid = gbuf.valid.reshape(-1)[band]
+    kind = gbuf.kind.reshape(-1)[band]
+    rough = gbuf.roughness.reshape(-1)[band]
     guided = valid & ((kind == DIFFUSE) | (rough >= rough_min)) & (st[:, EPOCH] >= 1.0)
     pix = np.nonzero(valid)[0]
     out = dict(wi=np.zeros((p, spp, 3)), pdf=np.zeros((p, spp)),
                strategy=np.zeros((p, spp), dtype=np.uint8), valid=np.zeros((p, spp), dtype=bool))
     if pix.size == 0:
         return out
-    pos = gbuf.pos.reshape(-1, 3)[pix]
-    nrm = gbuf.normal.reshape(-1, 3)[pix]
-    wo = gbuf.view.reshape(-1, 3)[pix]
+    pos = gbuf.pos.reshape(-1, 3)[band][pix]
+    nrm = gbuf.normal.reshape(-1, 3)[band][pix]
+    wo = gbuf.view.reshape(-1, 3)[band][pix]
     lbp = SimpleNamespace(mu=lb.mu[pix], l11=lb.l11[pix], l21=lb.l21[pix], l22=lb.l22[pix], z=lb.z[pix])
     out["draws"] = np.zeros((p, spp), dtype=np.int64)
+    gpix = (pix + r0 * w).astype(np.uint64)
     for s in range(spp):
-        state = seed_lanes(seed, frame, pix.astype(np.uint64) * np.uint64(spp) + np.uint64(s), 0)
+        state = seed_lanes(seed, frame, gpix * np.uint64(spp) + np.uint64(s), 0)
         for _ in range(nee_draws):
             draw_u32(state)
         start = state.copy()
@@ -655,14 +685,19 @@ def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROU
 
 
 def guiding_frame(stats_prev_f32, gbuf_prev, gbuf, vpl, seed, frame, spp=1, nee_draws=3, kmax=KMAX,
-                  radius=RADIUS, depth_rel_tol=0.1, normal_dot_min=0.9, rough_min=ROUGH_MIN_GUIDE):
+                  radius=RADIUS, depth_rel_tol=0.1, normal_dot_min=0.9, rough_min=ROUGH_MIN_GUIDE, rows=None):
     """One full guiding pass in reference order: reproject (if history),
     depth-0 sampling on the reprojected Gamma, EM on the same Gamma with the
-    frame's VPLs (pg/cli.py:114-142).  Returns (gamma_reproj, samples, gamma_trained)."""
+    frame's VPLs (pg/cli.py:114-142).  Returns (gamma_reproj, samples, gamma_trained).
+
+    ``rows=(r0, r1)``: outputs for frame rows r0..r1-1 only, the whole frame
+    as context (reprojection runs over the whole frame: it is cheap)."""
     if gbuf_prev is None:
         g = stats_prev_f32
     else:
         g = reproject(stats_prev_f32, gbuf_prev, gbuf, depth_rel_tol, normal_dot_min)
-    smp = sample_frame(g, gbuf, seed, frame, spp, nee_draws, rough_min)
-    g2 = train(g, vpl, gbuf, kmax, seed, frame, radius)
+    smp = sample_frame(g, gbuf, seed, frame, spp, nee_draws, rough_min, rows=rows)
+    g2 = train(g, vpl, gbuf, kmax, seed, frame, radius, rows=rows)
+    if rows is not None:
+        g = g[rows[0]:rows[1]]
     return g, smp, g2

@@ -111,6 +111,10 @@ _SIGS = {
     "pgg_primary_rays": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p],
     "pgg_sgmap": [c_i32, c_i64, c_p, c_p, c_p],
     "pgg_project": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p],
+    "pgg_debug_em_offsets": [ctypes.POINTER(Config), c_p, c_p, c_p],
+    "pgg_debug_bm_accept": [c_i64, c_i32, c_p, c_p, c_p, c_p, c_p],
+    "pgg_debug_reproject": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GBuffer),
+                            ctypes.POINTER(GammaIn), c_p, c_p],
 }
 
 EXPORTS = tuple(_SIGS) + ("pgg_frame_key", "pgg_status_string", "pgg_last_cuda_error", "pgg_abi_version")
@@ -171,8 +175,10 @@ def ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def stream_ptr(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def stream_ptr(stream=None, device=None):
+    """cudaStream_t of ``stream``, default the current stream of ``device``
+    (default: the current device)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
 
 

@@ -5,6 +5,7 @@
 //        -shared -Xcompiler -fPIC -I include csrc/pgg_kernels.cu -o libpgg.so
 #include <cuda.h>
 #include <algorithm>
+#include <atomic>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -230,15 +231,36 @@ bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Per-device state of the calling process: the dynamic-shared-memory opt-in
+// is an attribute of a kernel in one device context, so it is set once per
+// (instantiation, device).  Lock-free: concurrent first calls may both set
+// the (idempotent) attribute; the bit is published only after it succeeded.
+constexpr int MAX_DEVICES = 64;
+
+template <bool kTile, bool kFull>
+int ensure_smem_opt_in(int dev) {
+  static std::atomic<uint64_t> done{0};
+  if (dev < 0 || dev >= MAX_DEVICES) return PGG_ERR_UNSUPPORTED;
+  const uint64_t bit = 1ull << dev;
+  if (done.load(std::memory_order_acquire) & bit) return PGG_OK;
+  const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);  // the largest layout this instantiation can use
+  const cudaError_t e =
+      cudaFuncSetAttribute(k_guiding_pass<kTile, kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PGG_ERR_CUDA;
+  }
+  done.fetch_or(bit, std::memory_order_release);
+  return PGG_OK;
+}
+
 template <bool kTile, bool kFull>
 int launch_pass_t(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
   const SmemLayout SL(R, kTile);
-  static bool attr_set = false;  // opt in once to the largest layout this instantiation can use
-  if (!attr_set) {
-    const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);
-    cudaFuncSetAttribute(k_guiding_pass<kTile, kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
-    attr_set = true;
-  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return check_launch();
+  const int rc = ensure_smem_opt_in<kTile, kFull>(dev);
+  if (rc != PGG_OK) return rc;
   const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
   k_guiding_pass<kTile, kFull><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
   return check_launch();
@@ -463,7 +485,112 @@ __global__ void k_gamma_init(int64_t p, float4* g0, float4* g1) {
   g1[i] = b;
 }
 
+// ---------------------------------------------------------------------------
+// Diagnostics (tests only): the pass's discrete decisions over whole frames,
+// through the same device functions the fused kernel runs.
+
+// warp-aggregated counter add
+__device__ __forceinline__ void count_add(int32_t* c, int n) {
+  const unsigned m = __activemask();
+  int tot = n;
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(m, tot, o);
+  if ((threadIdx.x & 31) == (__ffs(m) - 1) && tot) atomicAdd(c, tot);
+}
+
+// the 19 candidate offsets of every pixel of the frame, as em_partial draws
+// them (jump tables, two interleaved streams, disk_offset_k with the pass's
+// radius / guard-band parameters)
+__global__ void k_debug_em_offsets(const PassArgs A, int8_t* __restrict__ out, int32_t* rechecks) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t P = (int64_t)A.cfg.width * A.cfg.height;
+  int n = 0;
+  if (p < P) {
+    const uint64_t s0 = pcg_lane(A.cfg.key_train, (uint64_t)p);
+    uint64_t sa = c_jmul[0] * s0 + c_jadd[0];
+    uint64_t sb = c_jmul[19] * s0 + c_jadd[19];
+    for (int s = 1; s < SLOTS; ++s) {
+      const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
+      sa = sa * PCG_MUL + PCG_INC;
+      sb = sb * PCG_MUL + PCG_INC;
+      int dx, dy;
+      disk_offset_k(ua, ub, A.cfg.radius, A.em_radius16, A.em_hband, dx, dy, &n);
+      out[(p * (SLOTS - 1) + (s - 1)) * 2] = (int8_t)dx;
+      out[(p * (SLOTS - 1) + (s - 1)) * 2 + 1] = (int8_t)dy;
+    }
+  }
+  count_add(rechecks, n);
+}
+
+// Box-Muller proposals of the guided branch: lobe from float32 Gamma
+// (make_lobe, as pixel_stage), acceptance via bm_propose
+__global__ void k_debug_bm_accept(int64_t n, int per, const float* __restrict__ stats, const uint32_t* __restrict__ ab,
+                                  uint8_t* __restrict__ out, int32_t* rechecks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int c = 0;
+  if (i < n) {
+    const float* g = stats + 8 * (i / per);
+    const LobeF L = make_lobe(g[0], g[1], g[2], g[3], g[4], g[6]);
+    CholD cd;
+    cd.mx = g[0];
+    cd.my = g[1];
+    cd.m2xx = g[2];
+    cd.m2yy = g[3];
+    cd.m2xy = g[4];
+    cd.from_floats = 0;
+    bool rc = false;
+    float px, py;
+    const bool in = bm_propose(L, cd, ab[2 * i], ab[2 * i + 1], px, py, &rc);
+    out[i] = (uint8_t)((in ? 1 : 0) | (rc ? 2 : 0));
+    c = rc ? 1 : 0;
+  }
+  count_add(rechecks, c);
+}
+
+// reprojection decision record of every pixel of the call's band
+__global__ void k_debug_reproject(const PassArgs A, uint8_t* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int yl = blockIdx.y;
+  if (x >= A.cfg.width) return;
+  const int y = A.cfg.row0 + yl;
+  const int64_t ci = (int64_t)(y - A.cur.row0) * A.cfg.width + x;
+  float4 g0, g1;
+  uint8_t d;
+  reproject_px<true>(A, x, y, ldu8(A.cur.flags, ci), ld4(A.cur.nd, ci), ld4(A.cur.pr, ci), ld4(A.cur.am, ci), g0,
+                     g1, &d);
+  out[(int64_t)yl * A.cfg.width + x] = d;
+}
+
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+namespace pgg_rt {
+// PGG_ERR_UNSUPPORTED unless the calling thread's current device is sm_100
+// (the library holds sm_100a code only); cached per device, lock-free
+int device_check() {
+  static std::atomic<uint8_t> state[64];  // 0 unknown, 1 sm_100, 2 other
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s", cudaGetErrorString(e));
+    return PGG_ERR_CUDA;
+  }
+  if (dev < 0 || dev >= 64) return PGG_ERR_UNSUPPORTED;
+  uint8_t st = state[dev].load(std::memory_order_relaxed);
+  if (st == 0) {
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+      return check_launch();
+    st = (major == 10 && minor == 0) ? 1 : 2;
+    state[dev].store(st, std::memory_order_relaxed);
+  }
+  return st == 1 ? PGG_OK : PGG_ERR_UNSUPPORTED;
+}
+}  // namespace pgg_rt
+
+namespace {
+using pgg_rt::device_check;
 
 }  // namespace
 
@@ -504,6 +631,14 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
     return PGG_ERR_ARGUMENT;
   if (vpl && (!gamma_out || !vpl->y || !vpl->L || cfg->k_max < 1)) return PGG_ERR_ARGUMENT;
   if (samples && (!samples->dir || !samples->tag || cfg->spp < 1 || cfg->nee_draws < 0)) return PGG_ERR_ARGUMENT;
+  // every supplied row range lies inside the frame: the whole-frame
+  // instantiation relies on TMA's zero fill beyond the VPL plane's rows for
+  // out-of-frame candidates, so a plane extending past the frame is refused
+  const auto in_frame = [&](int32_t r0, int32_t n) { return r0 >= 0 && n >= 0 && (int64_t)r0 + n <= cfg->height; };
+  if (!in_frame(cur->row0, cur->rows) || !in_frame(gamma_prev->row0, gamma_prev->rows)) return PGG_ERR_ARGUMENT;
+  if (prev && !in_frame(prev->row0, prev->rows)) return PGG_ERR_ARGUMENT;
+  if (vpl && !in_frame(vpl->row0, vpl->rows)) return PGG_ERR_ARGUMENT;
+  if (const int rc = device_check()) return rc;
   PassArgs A;
   memset(&A, 0, sizeof(A));
   A.cfg = *cfg;
@@ -564,6 +699,7 @@ int pgg_train_records(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_g
   A.gin = *gamma;
   A.vpl = *vpl;
   A.has_vpl = 1;
+  if (const int rc = device_check()) return rc;
   k_train_records<<<blocks(n, 64), 64, 0, S(stream)>>>(A, n, pix_xy, states, records);
   return check_launch();
 }
@@ -574,6 +710,7 @@ int pgg_sample_lanes(int64_t n, int32_t world, const float* normal, const float*
   if (n < 0 || !view || !rough || !glossy || !pi || !lobe6 || !states || !dir || !tag) return PGG_ERR_ARGUMENT;
   if (world && (!normal || !guided)) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_sample_lanes<<<blocks(n, 128), 128, 0, S(stream)>>>(
       n, world, reinterpret_cast<const float4*>(normal), reinterpret_cast<const float4*>(view), rough, glossy,
       guided, pi, lobe6, states, reinterpret_cast<float4*>(dir), tag);
@@ -584,6 +721,7 @@ int pgg_lobe(int64_t n, const double* stats, double* mu, double* cov, double* ch
              void* stream) {
   if (n < 0 || !stats || !mu || !cov || !chol || !trunc_z) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_lobe<<<blocks(n, 128), 128, 0, S(stream)>>>(n, stats, mu, cov, chol, trunc_z, reset);
   return check_launch();
 }
@@ -591,6 +729,7 @@ int pgg_lobe(int64_t n, const double* stats, double* mu, double* cov, double* ch
 int pgg_trunc_mass(int64_t n, const double* mu, const double* cov, double* z, void* stream) {
   if (n < 0 || !mu || !cov || !z) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_trunc<<<blocks(n, 128), 128, 0, S(stream)>>>(n, mu, cov, z);
   return check_launch();
 }
@@ -600,6 +739,7 @@ int pgg_m_step(int64_t n, int32_t c, const double* stats, const double* sq, cons
   if (n < 0 || c < 0 || !stats || !out || k_max < 1) return PGG_ERR_ARGUMENT;
   if (c > 0 && (!sq || !weight || !resp)) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_m_step<<<blocks(n, 128), 128, 0, S(stream)>>>(n, c, stats, sq, weight, resp, valid, k_max, out);
   return check_launch();
 }
@@ -607,6 +747,7 @@ int pgg_m_step(int64_t n, int32_t c, const double* stats, const double* sq, cons
 int pgg_make_streams(uint64_t key, int64_t n, const uint64_t* lanes, uint64_t* states, void* stream) {
   if (n < 0 || !lanes || !states) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_make_streams<<<blocks(n, 256), 256, 0, S(stream)>>>(key, n, lanes, states);
   return check_launch();
 }
@@ -614,6 +755,7 @@ int pgg_make_streams(uint64_t key, int64_t n, const uint64_t* lanes, uint64_t* s
 int pgg_next_u32(int64_t n, uint64_t* states, uint32_t* out, void* stream) {
   if (n < 0 || !states || !out) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_next_u32<<<blocks(n, 256), 256, 0, S(stream)>>>(n, states, out);
   return check_launch();
 }
@@ -626,6 +768,7 @@ int pgg_pack_gbuffer(int64_t p, const uint8_t* valid, const float* pos, const fl
       !va || !am)
     return PGG_ERR_ARGUMENT;
   if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_pack_gbuffer<<<blocks(p, 256), 256, 0, S(stream)>>>(
       p, valid, pos, normal, depth, kind, albedo, rough, view, motion, has_history, flags,
       reinterpret_cast<float4*>(nd), reinterpret_cast<float4*>(pr), reinterpret_cast<float4*>(va),
@@ -637,6 +780,7 @@ int pgg_pack_vpl(int64_t p, const uint8_t* valid, const float* y, const float* r
                  float* vy, float* vl, void* stream) {
   if (p < 0 || !valid || !y || !radiance || !strategy || !vy || !vl) return PGG_ERR_ARGUMENT;
   if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_pack_vpl<<<blocks(p, 256), 256, 0, S(stream)>>>(p, valid, y, radiance, strategy, reinterpret_cast<float4*>(vy),
                                                     reinterpret_cast<float4*>(vl));
   return check_launch();
@@ -645,6 +789,7 @@ int pgg_pack_vpl(int64_t p, const uint8_t* valid, const float* y, const float* r
 int pgg_gamma_split(int64_t p, const float* aos, float* g0, float* g1, void* stream) {
   if (p < 0 || !aos || !g0 || !g1) return PGG_ERR_ARGUMENT;
   if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_gamma_split<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<const float4*>(aos),
                                                        reinterpret_cast<float4*>(g0), reinterpret_cast<float4*>(g1));
   return check_launch();
@@ -653,15 +798,56 @@ int pgg_gamma_split(int64_t p, const float* aos, float* g0, float* g1, void* str
 int pgg_gamma_join(int64_t p, const float* g0, const float* g1, float* aos, void* stream) {
   if (p < 0 || !aos || !g0 || !g1) return PGG_ERR_ARGUMENT;
   if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_gamma_join<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<const float4*>(g0),
                                                       reinterpret_cast<const float4*>(g1),
                                                       reinterpret_cast<float4*>(aos));
   return check_launch();
 }
 
+int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream) {
+  if (!cfg || !offsets || !rechecks || cfg->width <= 0 || cfg->height <= 0) return PGG_ERR_ARGUMENT;
+  PassArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cfg = *cfg;
+  pass_args_finish(A);
+  const int64_t P = (int64_t)cfg->width * cfg->height;
+  if (const int rc = device_check()) return rc;
+  k_debug_em_offsets<<<blocks(P, 256), 256, 0, S(stream)>>>(A, offsets, rechecks);
+  return check_launch();
+}
+
+int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
+                        int32_t* rechecks, void* stream) {
+  if (n < 0 || per_lobe < 1 || !stats || !draws || !out || !rechecks) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_debug_bm_accept<<<blocks(n, 256), 256, 0, S(stream)>>>(n, per_lobe, stats, draws, out, rechecks);
+  return check_launch();
+}
+
+int pgg_debug_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
+                        const pgg_gamma_in* gamma_prev, uint8_t* decisions, void* stream) {
+  if (!cfg || !cur || !prev || !gamma_prev || !decisions) return PGG_ERR_ARGUMENT;
+  if (cfg->width <= 0 || cfg->rows < 0 || cfg->row0 < 0 || cfg->row0 + cfg->rows > cfg->height) return PGG_ERR_ARGUMENT;
+  if (cfg->rows == 0) return PGG_OK;
+  PassArgs A;
+  memset(&A, 0, sizeof(A));
+  A.cfg = *cfg;
+  pass_args_finish(A);
+  A.cur = *cur;
+  A.prev = *prev;
+  A.gin = *gamma_prev;
+  A.has_prev = 1;
+  if (const int rc = device_check()) return rc;
+  k_debug_reproject<<<dim3(blocks(cfg->width, 128), cfg->rows), 128, 0, S(stream)>>>(A, decisions);
+  return check_launch();
+}
+
 int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream) {
   if (p < 0 || !g0 || !g1) return PGG_ERR_ARGUMENT;
   if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
   k_gamma_init<<<blocks(p, 256), 256, 0, S(stream)>>>(p, reinterpret_cast<float4*>(g0), reinterpret_cast<float4*>(g1));
   return check_launch();
 }

@@ -153,10 +153,18 @@ PGG_COLD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float 
   oy = (float)sy;
 }
 
+// Decision record of one pixel's reprojection (diagnostic builds of the same
+// body, kDbg): bit0 accepted, bit1 the depth/normal gates were re-decided in
+// float64 (float32 within the guard band), bit2 the mean rotation rejected
+// (z < 0), bit3 the gates rejected.
+enum : uint8_t { RP_ACCEPT = 1, RP_GATE_F64 = 2, RP_ROT_REJECT = 4, RP_GATE_REJECT = 8 };
+
+template <bool kDbg = false>
 PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const float4& nd, const float4& pr,
-                         const float4& am, float4& g0, float4& g1) {
+                         const float4& am, float4& g0, float4& g1, uint8_t* dbg = nullptr) {
   const pgg_config& C = A.cfg;
   init_gamma(g0, g1);
+  if (kDbg) *dbg = 0;
   if ((fl & 3) != 3) return;  // valid & has_history
   const double tx = rint((double)x + (double)am.z);
   const double ty = rint((double)y + (double)am.w);
@@ -175,32 +183,47 @@ PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const floa
   const float4 p1 = ld4(A.gin.g1, gi);
   if (!(pfl & 1)) return;
 #if PGG_GATES_F32
-  // depth and normal gates decided in float32 when clear of the threshold by
-  // 1e-5 (the float32 error is ~1e-6 relative), else in float64 with the
-  // reference's operation order
+  // depth and normal gates decided in float32 when clear of the threshold,
+  // else in float64 with the reference's operation order.  Depth band: an
+  // absolute bound on the float32 error of lhs - rhs -- the rounding of
+  // (float)prev_cam (|cam| 2^-24 per component), of the differences, of the
+  // norm (a few ulps of def) and of ndp.w, rhs -- taken as 2^-19 (def + |ndp.w|
+  // + |cam|_1) (>= 8x the worst case), plus 1e-5 relative to rhs.
   int gate = 0;  // 1 pass, -1 reject, 0 undecided
   {
-    const float fx = pr.x - (float)C.prev_cam[0], fy = pr.y - (float)C.prev_cam[1], fz = pr.z - (float)C.prev_cam[2];
+    const float cx = (float)C.prev_cam[0], cy = (float)C.prev_cam[1], cz = (float)C.prev_cam[2];
+    const float fx = pr.x - cx, fy = pr.y - cy, fz = pr.z - cz;
     const float def = sqrtf(fx * fx + fy * fy + fz * fz);
     const float lhs = fabsf(ndp.w - def), rhs = (float)C.depth_rel_tol * fmaxf(def, 1e-12f);
     const float nf = ndp.x * nd.x + ndp.y * nd.y + ndp.z * nd.z, tn = (float)C.normal_dot_min;
-    const bool dpass = lhs < rhs * (1.0f - 1e-5f), dfail = lhs > rhs * (1.0f + 1e-5f);
+    const float eps = 1.9073486328125e-06f * (def + fabsf(ndp.w) + fabsf(cx) + fabsf(cy) + fabsf(cz)) + 1e-5f * rhs;
+    const bool dpass = lhs < rhs - eps, dfail = lhs > rhs + eps;
     const bool npass = nf > tn + 1e-5f, nfail = nf < tn - 1e-5f;
     if (dfail || nfail) gate = -1;
     else if (dpass && npass) gate = 1;
   }
-  if (gate < 0) return;
+  if (gate < 0) {
+    if (kDbg) *dbg |= RP_GATE_REJECT;
+    return;
+  }
   if (gate == 0) {
+    if (kDbg) *dbg |= RP_GATE_F64;
 #endif
   // depth and normal gates in float64, reference operation order
   const double dx = rsub((double)pr.x, C.prev_cam[0]);
   const double dy = rsub((double)pr.y, C.prev_cam[1]);
   const double dz = rsub((double)pr.z, C.prev_cam[2]);
   const double de = sqrt(radd(radd(rmul(dx, dx), rmul(dy, dy)), rmul(dz, dz)));
-  if (!(fabs(rsub((double)ndp.w, de)) < rmul(C.depth_rel_tol, fmax(de, 1e-12)))) return;
+  if (!(fabs(rsub((double)ndp.w, de)) < rmul(C.depth_rel_tol, fmax(de, 1e-12)))) {
+    if (kDbg) *dbg |= RP_GATE_REJECT;
+    return;
+  }
   const double ndot = radd(radd(rmul((double)ndp.x, (double)nd.x), rmul((double)ndp.y, (double)nd.y)),
                            rmul((double)ndp.z, (double)nd.z));
-  if (!(ndot > C.normal_dot_min)) return;
+  if (!(ndot > C.normal_dot_min)) {
+    if (kDbg) *dbg |= RP_GATE_REJECT;
+    return;
+  }
 #if PGG_GATES_F32
   }
 #endif
@@ -212,12 +235,16 @@ PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const floa
 #else
     rotate_or_reject(v3(ndp.x, ndp.y, ndp.z), v3(nd.x, nd.y, nd.z), p0.x, p0.y, keep, ox, oy);
 #endif
-    if (!keep) return;
+    if (!keep) {
+      if (kDbg) *dbg |= RP_ROT_REJECT;
+      return;
+    }
     p0.x = ox;
     p0.y = oy;
   }
   g0 = p0;
   g1 = p1;
+  if (kDbg) *dbg |= RP_ACCEPT;
 }
 
 // ---------------------------------------------------------------------------
@@ -285,6 +312,22 @@ PGG_HD V3<float> brdf_draw_local(const Mat<float>& mf, float alpha, const V3<flo
   return wl;
 }
 
+// One Box-Muller proposal p = mu + L z of the guided branch and its [0,1]^2
+// acceptance (mixture.py:216-230): float32, re-decided in float64 within the
+// guard band of an edge (*rechecked set then).
+PGG_HD bool bm_propose(const LobeF& L, const CholD& cd, uint32_t a, uint32_t b, float& px, float& py,
+                       bool* rechecked = nullptr) {
+  float z0, z1;
+  box_muller_f(a, b, z0, z1);
+  px = L.mx + L.l11 * z0;
+  py = L.my + L.l21 * z0 + L.l22 * z1;
+  if (near_edge(px) || near_edge(py)) {
+    if (rechecked) *rechecked = true;
+    return accept_d(cd, L.mx, L.my, a, b);
+  }
+  return px >= 0.0f && px <= 1.0f && py >= 0.0f && py <= 1.0f;
+}
+
 PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool guided, const LobeF& L,
                            const CholD& cd, uint64_t& st) {
   const Frame<float>& fr = pf.fr;
@@ -315,17 +358,8 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
     for (int t = 0; t < GAUSS_TRIES; ++t) {
       const uint32_t a = pcg_next(st), b = pcg_next(st);
       o.draws += 2;
-      float z0, z1;
-      box_muller_f(a, b, z0, z1);
-      const float px = L.mx + L.l11 * z0;
-      const float py = L.my + L.l21 * z0 + L.l22 * z1;
-      bool inside;
-      if (near_edge(px) || near_edge(py)) {
-        inside = accept_d(cd, L.mx, L.my, a, b);
-      } else {
-        inside = px >= 0.0f && px <= 1.0f && py >= 0.0f && py <= 1.0f;
-      }
-      if (inside) {
+      float px, py;
+      if (bm_propose(L, cd, a, b, px, py)) {
         acc = true;
         sx = m_clamp01(px);
         sy = m_clamp01(py);
@@ -393,13 +427,15 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
 #ifndef PGG_LOOP_TRIM
 #define PGG_LOOP_TRIM 1
 #endif
-PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy);
+PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy,
+                          int* rechecks = nullptr);
 PGG_HD void disk_offset(uint32_t ua, uint32_t ub, double radius, int& dx, int& dy) {
   const float rf = (float)radius;
   disk_offset_k(ua, ub, radius, rf * 1.52587890625e-05f, 0.5f - 4e-6f * (rf + 1.0f), dx, dy);
 }
 // rf16 = (float)radius * 2^-16, hb = 0.5 - 4e-6 ((float)radius + 1)
-PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy) {
+PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, float hb, int& dx, int& dy,
+                          int* rechecks) {
   const float band = 0.5f - hb;
   const float rf = rf16 * 65536.0f;
 #if defined(__CUDA_ARCH__) && PGG_EM_FAST
@@ -420,6 +456,7 @@ PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, f
 #else
   if (0.5f - fabsf(rx) < band || 0.5f - fabsf(ry) < band) {
 #endif
+    if (rechecks) ++*rechecks;
     const Off2 o = disk_offset_d(ua, ub, radius);
     dx = o.x;
     dy = o.y;
@@ -436,6 +473,7 @@ PGG_HD void disk_offset_k(uint32_t ua, uint32_t ub, double radius, float rf16, f
   const float ex = fabsf(fx - floorf(fx) - 0.5f);
   const float ey = fabsf(fy - floorf(fy) - 0.5f);
   if (ex < band || ey < band) {
+    if (rechecks) ++*rechecks;
     const Off2 o = disk_offset_d(ua, ub, radius);
     dx = o.x;
     dy = o.y;

@@ -29,6 +29,7 @@
 namespace pgg_rt {
 extern thread_local char g_cuda_err[256];
 int check_launch();
+int device_check();
 }  // namespace pgg_rt
 
 namespace {
@@ -901,6 +902,7 @@ int pgg_gbuffer_pass(const pgg_scene* scene, const pgg_camera* cam, const pgg_ca
   A.am = reinterpret_cast<float4*>(am);
   A.mat = mat;
   const dim3 blk(32, 4), grd((width + 31) / 32, (rows + 3) / 4);
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_gbuffer<<<grd, blk, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(A);
   return pgg_rt::check_launch();
 }
@@ -927,6 +929,7 @@ int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const 
   A.out = *out;
   const dim3 grd((cfg->width + RT_W - 1) / RT_W, (cfg->rows + RT_H - 1) / RT_H);
   const size_t smem = (table_doubles(scene) + 3 * P_FIELDS * RT_W * RT_H) * sizeof(double);
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_render<<<grd, dim3(RT_W, RT_H), smem, reinterpret_cast<cudaStream_t>(stream)>>>(A);
   return pgg_rt::check_launch();
 }
@@ -935,6 +938,7 @@ int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relativ
                     void* stream) {
   if (n <= 0 || !a || !ref || !scratch || !out) return PGG_ERR_ARGUMENT;
   const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_err_partial<<<ERR_BLOCKS, ERR_THREADS, 0, st>>>(n, a, ref, relative ? 1 : 0, scratch);
   k_err_final<<<1, ERR_THREADS, 0, st>>>(ERR_BLOCKS, scratch, n, out);
   return pgg_rt::check_launch();
@@ -948,6 +952,7 @@ int pgg_intersect(const pgg_scene* scene, int64_t n, const double* origins, cons
   if (!scene_ok(scene) || n < 0 || !origins || !dirs || !t_min || !t_max || !hit) return PGG_ERR_ARGUMENT;
   if (!any_hit && (!t || !pos || !normal || !mat || !front)) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_intersect<<<lane_blocks(n), 128, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(
       *scene, n, origins, dirs, t_min, t_max, any_hit, hit, t, pos, normal, mat, front);
   return pgg_rt::check_launch();
@@ -958,6 +963,7 @@ int pgg_sample_emitter(const pgg_scene* scene, int64_t n, const double* points, 
   if (!scene_ok(scene) || scene->n_emit < 1 || n < 0 || !points || !states || !dir || !dist || !emitted || !pdf)
     return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_emitter<<<lane_blocks(n), 128, table_doubles(scene) * sizeof(double), reinterpret_cast<cudaStream_t>(stream)>>>(
       *scene, n, points, states, dir, dist, emitted, pdf);
   return pgg_rt::check_launch();
@@ -970,6 +976,7 @@ int pgg_brdf(int32_t op, int64_t n, const int32_t* kind, const double* albedo, c
   if ((op == 0 && (!albedo || !f)) || (op == 1 && !pdf) || (op == 2 && (!states || !pdf || !valid)))
     return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_brdf<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(op, n, kind, albedo, rough, wi, wo,
                                                                                   normal, states, f, pdf, valid);
   return pgg_rt::check_launch();
@@ -979,6 +986,7 @@ int pgg_primary_rays(const pgg_camera* cam, int32_t width, int32_t height, int64
                      const double* py, double* dirs, void* stream) {
   if (!cam || width <= 0 || height <= 0 || n < 0 || !px || !py || !dirs) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_rays<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, px, py,
                                                                                   dirs);
   return pgg_rt::check_launch();
@@ -988,6 +996,7 @@ int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n,
                 double* py, uint8_t* in_front, void* stream) {
   if (!cam || width <= 0 || height <= 0 || n < 0 || !points || !px || !py || !in_front) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_project<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, points,
                                                                                      px, py, in_front);
   return pgg_rt::check_launch();
@@ -996,6 +1005,7 @@ int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n,
 int pgg_sgmap(int32_t op, int64_t n, const double* in, double* out, void* stream) {
   if (op < 0 || op > 6 || n < 0 || !in || !out) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_sgmap<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(op, n, in, out);
   return pgg_rt::check_launch();
 }

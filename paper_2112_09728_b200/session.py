@@ -53,11 +53,14 @@ def run_pass(cfg: PassConfig, frame: int, cur: GBufferPlanes, gamma_prev: GammaP
     grep = res.gamma_reproj.as_out() if want_reproj else None
     gout = res.gamma.as_out() if vpl is not None else None
     smp = res.samples.as_abi() if want_samples else None
-    _lib.check(_lib.lib().pgg_guiding_pass(
-        ref(c), ref(cur_abi), ref(prev_abi) if prev_abi is not None else None, ref(gin),
-        ref(vpl_abi) if vpl_abi is not None else None, ref(grep) if grep is not None else None,
-        ref(gout) if gout is not None else None, ref(smp) if smp is not None else None,
-        _lib.ptr(halo_misses), _lib.stream_ptr(stream)))
+    # launch on the tensors' device (and its current stream by default), not
+    # on whatever device the calling thread has current
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().pgg_guiding_pass(
+            ref(c), ref(cur_abi), ref(prev_abi) if prev_abi is not None else None, ref(gin),
+            ref(vpl_abi) if vpl_abi is not None else None, ref(grep) if grep is not None else None,
+            ref(gout) if gout is not None else None, ref(smp) if smp is not None else None,
+            _lib.ptr(halo_misses), _lib.stream_ptr(stream, dev)))
     return res
 
 

@@ -64,37 +64,66 @@ def test_trained_frame(cuda_dev):
     check_gamma(r.gamma.to_aos().cpu().numpy(), z["gamma_trained_r7"])
 
 
+def _ulp_perturbed_oracle_agreement(frames_ns, w, h, seed, pseed):
+    """The reference's own conditioning on this workload (SURVEY 8a basis,
+    drift.py): the oracle chain against the same chain with Gamma channels
+    0-5 nudged by one float32 ulp (random sign) after frame 0.  Returns the
+    final fraction of channels within 1e-4."""
+    a = O.fresh_stats(h * w).reshape(h, w, 8).astype(np.float32)
+    b = a.copy()
+    prev = None
+    rng = np.random.default_rng(pseed)
+    for f, (g, v) in enumerate(frames_ns):
+        _, _, a = O.guiding_frame(a, prev, g, v, seed, f, spp=1)
+        _, _, b = O.guiding_frame(b, prev, g, v, seed, f, spp=1)
+        if f == 0:
+            sgn = rng.choice([-1.0, 1.0], size=b[..., :6].shape).astype(np.float32)
+            b[..., :6] = np.nextafter(b[..., :6], b[..., :6] + sgn)
+        prev = g
+    return float(np.mean(gio.rel_err(b, a) <= 1e-4))
+
+
 def test_oracle_chain_160x120(cuda_dev):
     """4-frame fused chain on fresh synthetic inputs vs the oracle's chain
-    (trajectory tolerance)."""
+    (SURVEY 8a).  Every frame, the oracle is also run one step from the
+    GPU's own previous Gamma: that step must meet the single-kernel policy
+    (p99.99 <= 1e-4, max <= 1e-3, k exact) -- the kernel's own error.  The
+    chain itself must keep k exact on every pixel and max <= 1e-2, and >= 99.9 %
+    of channels within 1e-4 -- or, where the reference's own trajectory is
+    less stable than that, as close as the reference is to itself after a
+    one-ulp perturbation of Gamma (tools/chain_flips.py, profiles/
+    r2_chain_flips_160x120.json: at 160x120 / 4 frames the 1-ulp-perturbed
+    reference keeps 99.879-99.888 %, the GPU 99.881 %, with zero discrete
+    flips -- no reprojection, reset or k decision differs)."""
     from paper_2112_09728_b200 import synth
     from paper_2112_09728_b200.session import GuidingSession
     GammaPlanes, GBufferPlanes, PassConfig, VplPlanes, run_pass = _api()
-    from types import SimpleNamespace
     w, h, seed = 160, 120, 9
     frames = list(synth.sequence(w, h, 4, seed=seed))
     sess = GuidingSession(w, h, PassConfig(seed=seed, spp=1), device=cuda_dev)
     gam = O.fresh_stats(h * w).reshape(h, w, 8).astype(np.float32)
     prev_ns = None
-
-    def ns(d):
-        return SimpleNamespace(**{k: (v.numpy().astype(np.float64) if torch.is_tensor(v) and v.dtype == torch.float32
-                                      else (v.numpy() if torch.is_tensor(v) else v)) for k, v in d.items()})
-
+    frames_ns = []
     for f, (g, v) in enumerate(frames):
+        gpu_in = sess.gamma.to_aos().cpu().numpy()
         res = sess.step(GBufferPlanes.from_ref(g, device=cuda_dev), VplPlanes.from_ref(v, device=cuda_dev), f)
-        gn, vn = ns(g), ns(v)
+        gn, vn = _ns(g), _ns(v)
+        frames_ns.append((gn, vn))
         _, smp, gam = O.guiding_frame(gam, prev_ns, gn, vn, seed, f, spp=1)
+        _, asmp, astep = O.guiding_frame(gpu_in, prev_ns, gn, vn, seed, f, spp=1)   # re-anchored step
         prev_ns = gn
+        got = sess.gamma.to_aos().cpu().numpy()
+        check_gamma(got, astep)
         s = _samples(res, w * h, 1)
-        agree = np.mean(s["strategy"] == smp["strategy"])
-        assert agree >= 0.9999
+        check_samples(s, asmp["wi"], asmp["pdf"], asmp["strategy"], asmp["valid"])
+        np.testing.assert_array_equal(got[..., 7], gam[..., 7])  # k exact along the chain
     got = sess.gamma.to_aos().cpu().numpy()
     r = gio.rel_err(got, gam)
-    # chaotic trajectory (SURVEY 8a: a 1-ulp perturbation alone reaches p99.9
-    # 9.6e-5); measured on B200 after 4 frames: 99.89 % within 1e-4
-    assert np.mean(r <= 1e-4) >= 0.998 and r.max() <= 1e-2, (np.mean(r <= 1e-4), r.max())
-    assert np.mean(got[..., 7] == gam[..., 7]) >= 0.9999
+    frac = float(np.mean(r <= 1e-4))
+    assert r.max() <= 1e-2, r.max()
+    if frac < 0.999:
+        ref = min(_ulp_perturbed_oracle_agreement(frames_ns, w, h, seed, p) for p in (0, 1))
+        assert frac >= ref - 2e-4, (frac, ref)
 
 
 def test_1080p_determinism_and_bands(cuda_dev):
@@ -130,8 +159,8 @@ def test_1080p_determinism_and_bands(cuda_dev):
 def test_16_frame_trajectory_vs_oracle(cuda_dev):
     """SURVEY 8a N-frame policy over the BASELINE sequence length (16 frames,
     fresh Gamma, panning camera with disocclusions): >= 99.9 % of Gamma
-    channels within 1e-4 relative, max <= 1e-2, k equal on >= 99.99 % of
-    pixels, strategy tags >= 99.99 %, pdf p99.9 <= 1e-3."""
+    channels within 1e-4 relative, max <= 1e-2, k exact, strategy tags
+    >= 99.99 % (discrete masks of a drifting trajectory), pdf p99.9 <= 1e-3."""
     from types import SimpleNamespace
 
     from paper_2112_09728_b200 import synth
@@ -160,6 +189,60 @@ def test_16_frame_trajectory_vs_oracle(cuda_dev):
     got = sess.gamma.to_aos().cpu().numpy()
     r = gio.rel_err(got, gam)
     assert np.mean(r <= 1e-4) >= 0.999 and r.max() <= 1e-2, (np.mean(r <= 1e-4), r.max())
-    assert np.mean(got[..., 7] == gam[..., 7]) >= 0.9999
+    np.testing.assert_array_equal(got[..., 7], gam[..., 7])
     assert min(tags) >= 0.9999
     assert np.percentile(np.concatenate(pdf_err), 99.9) <= 1e-3
+
+
+def _ns(d):
+    from types import SimpleNamespace
+    return SimpleNamespace(**{k: (v.cpu().numpy().astype(np.float64) if torch.is_tensor(v) and v.dtype == torch.float32
+                                  else (v.cpu().numpy() if torch.is_tensor(v) else v)) for k, v in d.items()})
+
+
+BANDS_1080P = ((0, 48), (516, 564), (1032, 1080))  # top edge, middle, bottom edge
+
+
+def test_1080p_vs_oracle(cuda_dev):
+    """The benchmarked configuration (BASELINE configs[1]/[2]: 1920x1080,
+    1 spp, reproject + depth-0 sampling/pdf (MIS) + EM, disocclusions from
+    the panning camera and the hole pattern) against the CPU oracle on three
+    full-width row bands -- the top and bottom frame edges and the middle --
+    with the whole frame as context (pg/guide_buffers.py:262-283, 78-137;
+    pg/ptrace.py:161-220).  Gamma comes from four GPU frames of the bench
+    sequence (trained lobes: correlated, reset, k up to 4) and is fed to both
+    sides.  Single-kernel policy: Gamma p99.99 <= 1e-4, max <=
+    1e-3, k exact; samples: tags and validity exact, directions <= 1e-5,
+    pdf p99.99 <= 1e-4."""
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.session import GuidingSession
+    GammaPlanes, GBufferPlanes, PassConfig, VplPlanes, run_pass = _api()
+    w, h, seed, F = 1920, 1080, 0, 5
+    frames = list(synth.sequence(w, h, F, seed=seed, device=cuda_dev))
+    cfg = PassConfig(seed=seed, spp=1)
+    sess = GuidingSession(w, h, cfg, device=cuda_dev)
+    for f in range(F - 1):
+        g, v = frames[f]
+        sess.step(GBufferPlanes.from_ref(g, device=cuda_dev), VplPlanes.from_ref(v, device=cuda_dev), f)
+    gin = sess.gamma.to_aos().cpu().numpy()
+    (gp, _), (gc, vc) = frames[F - 2], frames[F - 1]
+    cur = GBufferPlanes.from_ref(gc, device=cuda_dev)
+    prev = GBufferPlanes.from_ref(gp, device=cuda_dev)
+    miss = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    r = run_pass(cfg, F - 1, cur, GammaPlanes.from_aos(gin, cuda_dev), prev=prev,
+                 vpl=VplPlanes.from_ref(vc, device=cuda_dev), want_reproj=True, halo_misses=miss)
+    got_rep = r.gamma_reproj.to_aos().cpu().numpy()
+    got = r.gamma.to_aos().cpu().numpy()
+    smp = _samples(r, w * h, 1)
+    gpn, gcn, vcn = _ns(gp), _ns(gc), _ns(vc)
+    rep = O.reproject(gin, gpn, gcn)
+    check_gamma(got_rep, rep)  # whole frame
+    assert int(miss.item()) == 0
+    valid = gcn.valid.astype(bool)
+    assert valid.mean() < 0.95 and (gin[..., 7] >= 1).mean() > 0.5  # disocclusions present, history trained
+    for r0, r1 in BANDS_1080P:
+        _, osmp, otr = O.guiding_frame(gin, gpn, gcn, vcn, seed, F - 1, spp=1, rows=(r0, r1))
+        check_gamma(got[r0:r1], otr)
+        band = slice(r0 * w, r1 * w)
+        check_samples({k: v[band] for k, v in smp.items()}, osmp["wi"], osmp["pdf"], osmp["strategy"],
+                      osmp["valid"])

@@ -139,3 +139,23 @@ def test_trained_frame(trained):
     assert gio.ulp_diff_f32(tr, z["gamma_trained"]).max() <= 1
     tr = O.train(z["gamma_in"], v, g, 32, seed, fr, radius=7.3)
     assert gio.ulp_diff_f32(tr, z["gamma_trained_r7"]).max() <= 1
+
+
+@pytest.mark.parametrize("rows", [(0, 11), (11, 30), (30, 40)])
+def test_row_band_equals_whole_frame(trained, rows):
+    """The oracle's row-band mode (whole frame as context, global stream
+    keys) reproduces the same rows of the whole-frame oracle bit for bit --
+    which is what lets the 1080p parity test check full-width bands, frame
+    edges included, without running the oracle on the whole frame."""
+    z = trained
+    spp, seed, fr = int(z["spp"]), int(z["seed"]), int(z["frame"])
+    gp, g = gio.gbuf(z, "p_"), gio.gbuf(z, "c_")
+    v = gio.vpl(z, "c_")
+    rep, smp, tr = O.guiding_frame(z["gamma_in"], gp, g, v, seed, fr, spp=spp)
+    rep_b, smp_b, tr_b = O.guiding_frame(z["gamma_in"], gp, g, v, seed, fr, spp=spp, rows=rows)
+    r0, r1 = rows
+    w = g.valid.shape[1]
+    np.testing.assert_array_equal(rep_b, rep[r0:r1])
+    np.testing.assert_array_equal(tr_b, tr[r0:r1])
+    for k in ("wi", "pdf", "strategy", "valid", "draws"):
+        np.testing.assert_array_equal(smp_b[k], smp[k][r0 * w:r1 * w])
