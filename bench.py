@@ -12,8 +12,13 @@ is needed.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one rank per GPU): every rank runs its own 1080p stream
-(8x batched 1080p of configs[4]: replicas, no collective; "scaling": "weak").
+N > 1: one rank per GPU under torch.distributed.run (bench.py re-launches
+itself that way when started without a torchrun environment; it exits with
+an error when fewer than N GPUs are visible or WORLD_SIZE != N).  Every rank
+runs its own 1080p stream (8x batched 1080p of configs[4]: replicas, no
+collective; "scaling": "weak"; value = N x frames / max-over-ranks time), and
+the same line carries "bands_4k4spp": one 4K 4 spp frame split into N row
+bands with the overlapped NCCL halo exchange (configs[3], strong scaling).
 --impl reference times the CPU reference path (the oracle port of pgtrace,
 oracle/pgg_oracle.py) on the host cores, rank 0 only.
 """
@@ -52,7 +57,20 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-frame-loop", action="store_true")
     ap.add_argument("--bands", action="store_true", help="row-band path even at N=1 (exercises the NCCL code)")
+    ap.add_argument("--no-bands", action="store_true", help="N>1: skip the 4K 4 spp row-band leg")
     return ap.parse_args()
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment:
+    re-exec this script as N ranks of torch.distributed.run on this node."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def ncu_capture(workload, key):
@@ -351,9 +369,11 @@ def bench_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def bench_bands(args, rank, world, local_rank):
+def bench_bands(args, rank, world, local_rank, w, h, spp, steps, warmup, workload):
     """configs[3]/[4] at N GPUs: one frame split into N row bands, NCCL halo
-    exchange of the EM / reprojection halos every frame (strong scaling)."""
+    exchange of the EM / reprojection halos every frame, overlapped with the
+    band's interior rows (strong scaling).  Returns rank 0's record (None on
+    the other ranks)."""
     import torch
     import torch.distributed as dist
 
@@ -363,11 +383,11 @@ def bench_bands(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    cfg = PassConfig(seed=0, spp=args.spp)
-    band = BandedGuiding(W, H, cfg, rank=rank, world=world, device=dev, max_motion_rows=8)
+    cfg = PassConfig(seed=0, spp=spp)
+    band = BandedGuiding(w, h, cfg, rank=rank, world=world, device=dev, max_motion_rows=8)
     eg, ev = band.ext_g, band.ext_v
     frames = []
-    for g, v in synth.sequence(W, H, SEQ, seed=0, device=dev):
+    for g, v in synth.sequence(w, h, SEQ, seed=0, device=dev):
         full_g, full_v = GBufferPlanes.from_ref(g, device=dev), VplPlanes.from_ref(v, device=dev)
         gb, vp = band.extended_planes()
         for name in ("flags", "nd", "pr", "va", "am"):
@@ -387,39 +407,41 @@ def bench_bands(args, rank, world, local_rank):
         band.step(i % SEQ, gbuf=gb, vpl=vp)
         state["i"] = i + 1
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     dist.barrier()
+    torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         clk.wait_ready()
         h0 = time.monotonic()
         t0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         t1.record(stream)
         torch.cuda.synchronize(dev)
         clk.mark(h0, time.monotonic())
     total = torch.tensor([t0.elapsed_time(t1)], device=dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
-    ms = float(total.item()) / args.steps
-    if rank == 0:
-        peak, peak_kind = peaks()
-        bpx = BYTES_PER_PX + BYTES_PER_EXTRA_SPP * (args.spp - 1)
-        achieved = bpx * W * H / (ms * 1e-3) / 1e9 / world
-        line = {"metric": f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)", "value": W * H / (ms * 1e-3) / 1e6,
-                "unit": "Mpixels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic",
-                "config": {"workload": WORKLOADS[args.workload][3] + ", row bands + NCCL halo exchange",
-                           "parallelism": f"bands{world}"},
-                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": ncu_traffic(args.workload) if world == 1 else None,
-                             "peak_kind": peak_kind, "note": "per GPU, step time incl. halo exchange"},
-                "clocks": clk.summary(), "gpu_launches": args.steps, "e2e": None, "cpu_baseline": None,
-                "halo_misses": band.halo_misses()}
-        print(json.dumps(line), flush=True)
+    misses = band.halo_misses()
+    ms = float(total.item()) / steps
+    if rank != 0:
+        return None
+    peak, peak_kind = peaks()
+    bpx = BYTES_PER_PX + BYTES_PER_EXTRA_SPP * (spp - 1)
+    achieved = bpx * w * h / (ms * 1e-3) / 1e9 / world
+    return {"metric": f"guiding-pass Mpixels/s ({w}x{h}, {spp} spp)", "value": w * h / (ms * 1e-3) / 1e6,
+            "unit": "Mpixels/s", "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms,
+            "ms_per_frame": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[workload][3] + ", row bands + NCCL halo exchange",
+                       "parallelism": f"bands{world}",
+                       "l2": "inputs larger than L2 (16 frames rotating); no flush"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(workload) if world == 1 else None,
+                         "peak_kind": peak_kind, "note": "per GPU, step time incl. halo exchange"},
+            "clocks": clk.summary(), "gpu_launches": steps * (2 if world > 1 else 1), "halo_misses": misses}
 
 
 def bench_ours(args, rank, world, local_rank):
@@ -483,12 +505,22 @@ def bench_ours(args, rank, world, local_rank):
     achieved = bpx * W * H / (kavg * 1e-3) / 1e9
 
     wstats = workload_stats(frames, state["g"]) if rank == 0 else {}
+    gpu_launches = args.steps
     floop = None
     if rank == 0 and world == 1 and args.workload == "1080p" and not args.no_frame_loop:
         floop = bench_frame_loop(dev)
     e2e = None
     if not args.no_e2e:
         e2e = bench_e2e(args, frames, cfg, dev, world)
+    bands = None
+    if world > 1 and not args.no_bands:
+        # the strong-scaling leg of the same run: one 4K 4 spp frame over N
+        # row bands with the NCCL halo exchange (BASELINE configs[3])
+        frames.clear()
+        torch.cuda.empty_cache()
+        w4, h4, spp4, _ = WORKLOADS["4k4spp"]
+        bands = bench_bands(args, rank, world, local_rank, w4, h4, spp4, max(8, min(args.steps, 32)),
+                            max(3, args.warmup), "4k4spp")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         px, secs, thr = run_cpu_reference(rows_per_thread=216, threads=1)
@@ -515,8 +547,10 @@ def bench_ours(args, rank, world, local_rank):
                              "issue": issue_roofline(args.workload, kavg),
                              "kernel": "k_guiding_pass (fused)"},
                 "clocks": clk.summary(),
-                "gpu_launches": args.steps,
+                "gpu_launches": gpu_launches,
                 "e2e": e2e, "cpu_baseline": cpu, "frame_loop": floop}
+        if bands is not None:
+            line["bands_4k4spp"] = bands
         print(json.dumps(line), flush=True)
 
 
@@ -634,6 +668,11 @@ def bench_e2e(args, frames, cfg, dev, world):
     b.record(s_out)
     torch.cuda.synchronize(dev)
     ms = a.elapsed_time(b) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     return {"value": world * W * H / (ms * 1e-3) / 1e6, "unit": "Mpixels/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
             "path": "pinned host packed planes -> H2D -> pgg_guiding_pass -> pgg_gamma_join + samples -> D2H, "
@@ -646,21 +685,37 @@ def main():
     W, H, spp0, _ = WORKLOADS[args.workload]
     if args.spp is None:
         args.spp = spp0
+    if args.gpus < 1:
+        sys.exit(f"bench.py: --gpus must be >= 1 (got {args.gpus})")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl != "reference":
+            import torch
+            n = torch.cuda.device_count()
+            if n < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} requested but only {n} CUDA device(s) are visible")
+        relaunch_under_torchrun(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: rank {rank}: WORLD_SIZE={world} but --gpus {args.gpus}")
     if args.impl == "reference":
         bench_reference(args, rank, world)
         return
     import torch
     import torch.distributed as dist
+    if torch.cuda.device_count() <= local_rank:
+        sys.exit(f"bench.py: rank {rank}: LOCAL_RANK={local_rank} but only {torch.cuda.device_count()} "
+                 "CUDA device(s) are visible")
     use_dist = world > 1 or args.bands
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
     __graft_entry__.build()
     if args.bands or (world > 1 and args.workload != "1080p"):
-        bench_bands(args, rank, world, local_rank)
+        line = bench_bands(args, rank, world, local_rank, W, H, args.spp, args.steps, args.warmup, args.workload)
+        if line is not None:
+            print(json.dumps(line), flush=True)
     else:
         bench_ours(args, rank, world, local_rank)
     if use_dist:
