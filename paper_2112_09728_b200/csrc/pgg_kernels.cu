@@ -508,6 +508,27 @@ __global__ void k_debug_em_offsets(const PassArgs A, int8_t* __restrict__ out, i
     const uint64_t s0 = pcg_lane(A.cfg.key_train, (uint64_t)p);
     uint64_t sa = c_jmul[0] * s0 + c_jadd[0];
     uint64_t sb = c_jmul[19] * s0 + c_jadd[19];
+#if defined(__CUDA_ARCH__) && PGG_EM_PAIR
+    // the pass's paired path (em_partial) computes each slot's offset with
+    // disk_offset_k2; the partner slot does not change a slot's arithmetic
+    for (int s = 1; s < SLOTS; s += 2) {
+      const uint32_t ua0 = pcg_out(sa), ub0 = pcg_out(sb);
+      sa = sa * PCG_MUL + PCG_INC;
+      sb = sb * PCG_MUL + PCG_INC;
+      const uint32_t ua1 = pcg_out(sa), ub1 = pcg_out(sb);
+      sa = sa * PCG_MUL + PCG_INC;
+      sb = sb * PCG_MUL + PCG_INC;
+      int dx0, dy0, dx1, dy1, m0 = 0, m1 = 0;
+      disk_offset_k2(ua0, ub0, ua1, ub1, A.cfg.radius, A.em_radius16, A.em_hband, dx0, dy0, dx1, dy1, &m0, &m1);
+      n += m0 + (s + 1 < SLOTS ? m1 : 0);  // slot 20 does not exist: the last pair's partner is masked
+      out[(p * (SLOTS - 1) + (s - 1)) * 2] = (int8_t)dx0;
+      out[(p * (SLOTS - 1) + (s - 1)) * 2 + 1] = (int8_t)dy0;
+      if (s + 1 < SLOTS) {
+        out[(p * (SLOTS - 1) + s) * 2] = (int8_t)dx1;
+        out[(p * (SLOTS - 1) + s) * 2 + 1] = (int8_t)dy1;
+      }
+    }
+#else
     for (int s = 1; s < SLOTS; ++s) {
       const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
       sa = sa * PCG_MUL + PCG_INC;
@@ -517,6 +538,7 @@ __global__ void k_debug_em_offsets(const PassArgs A, int8_t* __restrict__ out, i
       out[(p * (SLOTS - 1) + (s - 1)) * 2] = (int8_t)dx;
       out[(p * (SLOTS - 1) + (s - 1)) * 2 + 1] = (int8_t)dy;
     }
+#endif
   }
   count_add(rechecks, n);
 }

@@ -292,6 +292,14 @@ template <class T> struct K {
 
 constexpr uint64_t PCG_MUL = 6364136223846793005ULL;
 constexpr uint64_t PCG_INC = 1442695040888963407ULL;
+// PCG_MUL^-1 mod 2^64 (Newton: each step doubles the correct low bits)
+constexpr uint64_t inv_mod64(uint64_t a) {
+  uint64_t x = a;  // a odd: a * a = 1 mod 8
+  for (int i = 0; i < 5; ++i) x *= 2 - a * x;
+  return x;
+}
+constexpr uint64_t PCG_MUL_INV = inv_mod64(PCG_MUL);
+static_assert(PCG_MUL * PCG_MUL_INV == 1, "PCG multiplier inverse");
 
 PGG_HD uint64_t splitmix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ULL;

@@ -734,6 +734,54 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, i
 // guide_buffers.py:144-145) and rounds the disk offset.
 // kFull: the VPL planes cover the whole frame (every launch but a row band's),
 // so no candidate can miss them and no halo misses are counted.
+#ifndef PGG_EM_PAIR
+// 2: all candidate slots in pairs (0, 1), (2, 3), ... with the record math in
+// packed FP32 (FFMA2 / FMUL2 / FADD2, pgg_pair.cuh).  Measured on B200 (1080p
+// bench): 5.7 % fewer warp-instructions but issue utilisation 70.5 -> 63.7 %
+// (long-scoreboard, instruction-fetch and math-pipe-throttle stalls up),
+// 0.4967 vs 0.4725 ms -- slower, also at 2 blocks/SM without spills
+// (0.4966 ms); off.  DESIGN.md section 4.
+#define PGG_EM_PAIR 0
+#endif
+}  // namespace pgg
+#include "pgg_pair.cuh"
+namespace pgg {
+
+#ifdef __CUDA_ARCH__
+// disk_offset_k for two slots: the float32 arithmetic packed (FFMA2 / FADD2),
+// sin / cos / sqrt per slot on MUFU, the same guard band and float64
+// re-decision per slot
+PGG_PI void disk_offset_k2(uint32_t ua0, uint32_t ub0, uint32_t ua1, uint32_t ub1, double radius, float rf16,
+                           float hb, int& dx0, int& dy0, int& dx1, int& dy1, int* rechecks0 = nullptr,
+                           int* rechecks1 = nullptr) {
+  const F2 r = f2(f_sqrt_mufu((float)ua0), f_sqrt_mufu((float)ua1)) * rf16;
+  const float th0 = (float)(int32_t)ub0 * 1.4629180792671596e-09f;
+  const float th1 = (float)(int32_t)ub1 * 1.4629180792671596e-09f;
+  const F2 fx = r * f2(__cosf(th0), __cosf(th1)), fy = r * f2(__sinf(th0), __sinf(th1));
+  const float kM = 12582912.0f;  // 1.5 * 2^23: x + kM rounds x to the nearest integer (even on ties)
+  const F2 tx = fx + kM, ty = fy + kM;
+  const F2 rx = fx - (tx - kM), ry = fy - (ty - kM);
+  if (fabsf(lo(rx)) > hb || fabsf(lo(ry)) > hb) {
+    if (rechecks0) ++*rechecks0;
+    const Off2 o = disk_offset_d(ua0, ub0, radius);
+    dx0 = o.x;
+    dy0 = o.y;
+  } else {
+    dx0 = __float_as_int(lo(tx)) - 0x4B400000;
+    dy0 = __float_as_int(lo(ty)) - 0x4B400000;
+  }
+  if (fabsf(hi(rx)) > hb || fabsf(hi(ry)) > hb) {
+    if (rechecks1) ++*rechecks1;
+    const Off2 o = disk_offset_d(ua1, ub1, radius);
+    dx1 = o.x;
+    dy1 = o.y;
+  } else {
+    dx1 = __float_as_int(hi(tx)) - 0x4B400000;
+    dy1 = __float_as_int(hi(ty)) - 0x4B400000;
+  }
+}
+#endif
+
 template <bool kFull = false, class VS>
 PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, int y, const uint64_t* jmul,
                        const uint64_t* jadd, float* acc) {
@@ -752,6 +800,49 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     const float4 nd = ld4(A.cur.nd, (int64_t)(y - A.cur.row0) * C.width + x);
     return v3(nd.x, nd.y, nd.z);
   };
+#if defined(__CUDA_ARCH__) && PGG_EM_PAIR == 2
+  {
+    // every slot in pairs (0, 1), (2, 3), ...; slot 0 is the pixel's own VPL
+    // (offset 0, no draws): the streams start one step before draws 0 / 19
+    constexpr bool kNoBounds2 = PGG_TILE_OOB && kFull && VS::kZeroOOB;
+    uint64_t sa = (S.s0 - PCG_INC) * PCG_MUL_INV;
+    uint64_t sb = jmul[18] * S.s0 + jadd[18];
+    int misses = 0;
+    F2 acc2[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc2[k] = f2s(0.0f);
+    for (int s = 0; s < S.nb; s += 2) {
+      const uint32_t ua0 = pcg_out(sa), ub0 = pcg_out(sb);
+      sa = sa * PCG_MUL + PCG_INC;
+      sb = sb * PCG_MUL + PCG_INC;
+      const uint32_t ua1 = pcg_out(sa), ub1 = pcg_out(sb);
+      sa = sa * PCG_MUL + PCG_INC;
+      sb = sb * PCG_MUL + PCG_INC;
+      const bool has1 = s + 1 < S.nb;
+      int dx0, dy0, dx1, dy1;
+      disk_offset_k2(ua0, ub0, ua1, ub1, C.radius, A.em_radius16, A.em_hband, dx0, dy0, dx1, dy1);
+      if (s == 0) dx0 = dy0 = 0;  // self
+      const int cx0 = x + dx0, cy0 = y + dy0, cx1 = x + dx1, cy1 = y + dy1;
+      const bool inf0 = kNoBounds2 || ((unsigned)cx0 < W && (unsigned)cy0 < H);
+      const bool inf1 = kNoBounds2 || ((unsigned)cx1 < W && (unsigned)cy1 < H);
+      const bool inv0 = kFull || (unsigned)(cy0 - vr0) < vrows;
+      const bool inv1 = kFull || (unsigned)(cy1 - vr0) < vrows;
+      if (!kFull) misses += ((inf0 && !inv0) ? 1 : 0) + ((has1 && inf1 && !inv1) ? 1 : 0);
+      bool ok0 = inf0 && inv0;
+      bool ok1 = has1 && inf1 && inv1;
+      const auto idx0 = (kNoBounds2 || ok0) ? base + (decltype(base))dy0 * stride + dx0 : base;
+      const auto idx1 = (kNoBounds2 || ok1) ? base + (decltype(base))dy1 * stride + dx1 : base;
+      const float4 vy0 = V.y_at(idx0), vy1 = V.y_at(idx1);
+      ok0 = ok0 && vy0.w != 0.0f;  // VPL invalid or not BRDF-strategy
+      ok1 = ok1 && vy1.w != 0.0f;
+      em_accumulate2(S, vy0, vy1, V, idx0, idx1, ok0, ok1, acc2, n_raw);
+    }
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc[k] += lo(acc2[k]) + hi(acc2[k]);
+    if (!kFull && misses) count_miss(A.halo_misses, misses);
+    return;
+  }
+#endif
   {
     const float4 vy = V.y_at(base);
     em_accumulate(S, vy, V, base, vy.w != 0.0f, acc, n_raw);
@@ -761,6 +852,10 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   uint64_t sa = jmul[0] * S.s0 + jadd[0];     // draw 0: u1 of slot 1
   uint64_t sb = jmul[19] * S.s0 + jadd[19];   // draw 19: u2 of slot 1
   int misses = 0;  // in-frame candidates outside the supplied VPL rows (halo misses)
+  // whole-frame VPLs staged by TMA: every candidate (|d| <= R) lies in the
+  // tile and those outside the frame read TMA's zero fill, i.e. an invalid
+  // VPL (w = 0) -- the reference's "out of frame -> unused" without a test
+  constexpr bool kNoBounds = PGG_TILE_OOB && kFull && VS::kZeroOOB;
   for (; s < S.nb; ++s) {
     const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
     sa = sa * PCG_MUL + PCG_INC;
@@ -768,10 +863,6 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
     int dx, dy;
     disk_offset_k(ua, ub, C.radius, A.em_radius16, A.em_hband, dx, dy);
     const int cx = x + dx, cy = y + dy;
-    // whole-frame VPLs staged by TMA: every candidate (|d| <= R) lies in the
-    // tile and those outside the frame read TMA's zero fill, i.e. an invalid
-    // VPL (w = 0) -- the reference's "out of frame -> unused" without a test
-    constexpr bool kNoBounds = PGG_TILE_OOB && kFull && VS::kZeroOOB;
     const bool in_frame = kNoBounds || ((unsigned)cx < W && (unsigned)cy < H);
     const bool in_vpl = kFull || (unsigned)(cy - vr0) < vrows;
     if (!kFull) misses += (in_frame && !in_vpl) ? 1 : 0;
