@@ -16,6 +16,10 @@
  *                          mixture.sample_mixture       mixture.py:193-259 on
  *                          caller-owned PCG32 states (in/out)
  *   pgg_lobe ............. mixture.lobe_from_stats      mixture.py:129-155
+ *   pgg_mixture_lanes .... mixture.gaussian_pdf_square / mixture_pdf / box_muller /
+ *                          e_step_responsibility / neighbor_count  mixture.py:158-190, 262-273, 324-328
+ *   pgg_sample_gauss ..... the Gaussian branch of mixture.sample_mixture (mixture.py:208-235)
+ *                          for callers with their own BRDF callbacks
  *   pgg_trunc_mass ....... mixture.truncation_mass      mixture.py:84-126
  *   pgg_m_step ........... mixture.m_step_update        mixture.py:276-321
  *   pgg_make_streams ..... rng.make_streams             rng.py:25-39
@@ -308,6 +312,25 @@ int pgg_image_error(int64_t n, const float* a, const float* ref, int32_t relativ
 const char* pgg_status_string(int status);
 const char* pgg_last_cuda_error(void);
 int pgg_abi_version(void);
+
+/* mixture.py's remaining lane functions in float64 (device arrays, n lanes):
+ *   op 0 gaussian_pdf_square  a = mu (n,2), b = chol (n,2,2), c = trunc_z (n), d = p (n,2)  mixture.py:158-169
+ *   op 1 box_muller           a = u1, b = u2 -> out0 = z0, out1 = z1                       mixture.py:185-190
+ *   op 2 e_step_responsibility a = pi, b = gauss pdf, c = brdf pdf                          mixture.py:262-273
+ *   op 3 neighbor_count       a = k, k_max -> out0 = N (as double)                          mixture.py:324-328
+ *   op 4 mixture_pdf          a = pi, b = per lane (mu_x, mu_y, l11, 0, l21, l22, trunc_z) (n,7),
+ *                             c = square point of the direction (n,2), d = brdf pdf         mixture.py:172-182
+ * (e is unused; out1 only for op 1) */
+int pgg_mixture_lanes(int32_t op, int64_t n, const double* a, const double* b, const double* c, const double* d,
+                      const double* e, double* out0, double* out1, int32_t k_max, void* stream);
+
+/* Gaussian branch of mixture.sample_mixture (mixture.py:208-235) in float64
+ * for callers that keep the reference's Python BRDF callbacks: per lane a
+ * zeta draw (< pi) and up to 16 Box-Muller tries on `states` (advanced in
+ * place); writes the accepted square point (n,2) and accepted[i] in {0,1}.
+ * The BRDF fallback and pdf are the caller's (pg/ptrace.py:201-208). */
+int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double* chol, uint64_t* states, double* sq,
+                     uint8_t* accepted, void* stream);
 
 /* Diagnostics (test-only; not on the product path).  Each runs the device
  * functions of pgg_guiding_pass over a whole frame / batch and records the

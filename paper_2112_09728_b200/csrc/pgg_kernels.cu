@@ -486,6 +486,94 @@ __global__ void k_gamma_init(int64_t p, float4* g0, float4* g1) {
 }
 
 // ---------------------------------------------------------------------------
+// The remaining mixture.py entry points as float64 lane kernels, with the
+// reference's operation order (no FMA contraction: rmul / radd / rsub).
+
+enum MixOp { MIX_GAUSS_PDF = 0, MIX_BOX_MULLER = 1, MIX_E_STEP = 2, MIX_NEIGHBORS = 3, MIX_PDF = 4 };
+
+// gaussian_pdf_square (mixture.py:158-169): mu (2), chol (4: l11, 0, l21, l22), z
+__device__ __forceinline__ double gauss_pdf_d(const double* mu, const double* ch, double z, double px, double py) {
+  const double l11 = ch[0], l21 = ch[2], l22 = ch[3];
+  const double z1 = rsub(px, mu[0]) / l11;
+  const double z2 = rsub(rsub(py, mu[1]), rmul(l21, z1)) / l22;
+  const double e = exp(rmul(-0.5, radd(rmul(z1, z1), rmul(z2, z2))));
+  return rmul(e, 1.0 / rmul(rmul(2.0 * K<double>::pi, l11), l22)) / z;
+}
+
+__global__ void k_mixture_lanes(int op, int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                                const double* __restrict__ c, const double* __restrict__ d,
+                                const double* __restrict__ e, double* __restrict__ o0, double* __restrict__ o1,
+                                int kmax) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  switch (op) {
+    case MIX_GAUSS_PDF:  // a = mu (n,2), b = chol (n,4), c = z (n), d = p (n,2)
+      o0[i] = gauss_pdf_d(a + 2 * i, b + 4 * i, c[i], d[2 * i], d[2 * i + 1]);
+      break;
+    case MIX_BOX_MULLER: {  // a = u1, b = u2 (mixture.py:185-190)
+      const double u1 = fmax(a[i], 1e-12);
+      const double r = sqrt(rmul(-2.0, log(u1)));
+      const double ang = rmul(2.0 * K<double>::pi, b[i]);
+      o0[i] = rmul(r, cos(ang));
+      o1[i] = rmul(r, sin(ang));
+      break;
+    }
+    case MIX_E_STEP: {  // a = pi, b = gauss pdf, c = brdf pdf (mixture.py:262-273)
+      const double num = rmul(a[i], b[i]);
+      const double den = radd(num, rmul(rsub(1.0, a[i]), c[i]));
+      o0[i] = den > 0.0 ? num / den : 0.0;
+      break;
+    }
+    case MIX_NEIGHBORS: {  // a = k (mixture.py:324-328); integer result stored as double
+      const double kk = fmin(a[i], (double)kmax);
+      o0[i] = floor(radd(radd(rmul(rsub(1.0, kk / (double)kmax), 15.0), 5.0), 0.5));
+      break;
+    }
+    case MIX_PDF: {  // a = pi, b = mu|chol|z packed (n,7), c = square point (n,2), d = brdf pdf (mixture.py:172-182)
+      const double* L = b + 7 * i;
+      const double g = gauss_pdf_d(L, L + 2, L[6], c[2 * i], c[2 * i + 1]) / (2.0 * K<double>::pi);
+      o0[i] = radd(rmul(a[i], g), rmul(rsub(1.0, a[i]), d[i]));
+      break;
+    }
+  }
+}
+
+// Gaussian branch of sample_mixture (mixture.py:208-235) in float64 for
+// callers with their own BRDF callbacks: zeta draw, up to 16 Box-Muller
+// tries on the lane's stream; out: accepted flag, square point
+__global__ void k_sample_gauss(int64_t n, const double* __restrict__ pi, const double* __restrict__ mu,
+                               const double* __restrict__ chol, uint64_t* __restrict__ states, double* __restrict__ sq,
+                               uint8_t* __restrict__ acc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t st = states[i];
+  const uint32_t uz = pcg_next(st);
+  uint8_t hit = 0;
+  double px = 0.0, py = 0.0;
+  if (u01d(uz) < pi[i]) {
+    const double mx = mu[2 * i], my = mu[2 * i + 1];
+    const double l11 = chol[4 * i], l21 = chol[4 * i + 2], l22 = chol[4 * i + 3];
+    for (int t = 0; t < GAUSS_TRIES; ++t) {
+      const uint32_t ua = pcg_next(st), ub = pcg_next(st);
+      double z0, z1;
+      box_muller_d(ua, ub, z0, z1);
+      const double qx = radd(mx, rmul(l11, z0));
+      const double qy = radd(radd(my, rmul(l21, z0)), rmul(l22, z1));
+      if (qx >= 0.0 && qx <= 1.0 && qy >= 0.0 && qy <= 1.0) {
+        hit = 1;
+        px = qx;
+        py = qy;
+        break;
+      }
+    }
+  }
+  states[i] = st;
+  sq[2 * i] = px;
+  sq[2 * i + 1] = py;
+  acc[i] = hit;
+}
+
+// ---------------------------------------------------------------------------
 // Diagnostics (tests only): the pass's discrete decisions over whole frames,
 // through the same device functions the fused kernel runs.
 
@@ -863,6 +951,28 @@ int pgg_debug_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg
   A.has_prev = 1;
   if (const int rc = device_check()) return rc;
   k_debug_reproject<<<dim3(blocks(cfg->width, 128), cfg->rows), 128, 0, S(stream)>>>(A, decisions);
+  return check_launch();
+}
+
+int pgg_mixture_lanes(int32_t op, int64_t n, const double* a, const double* b, const double* c, const double* d,
+                      const double* e, double* out0, double* out1, int32_t k_max, void* stream) {
+  if (n < 0 || op < 0 || op > 4 || !a || !out0) return PGG_ERR_ARGUMENT;
+  if ((op == MIX_GAUSS_PDF || op == MIX_PDF) && (!b || !c || !d)) return PGG_ERR_ARGUMENT;
+  if (op == MIX_BOX_MULLER && (!b || !out1)) return PGG_ERR_ARGUMENT;
+  if (op == MIX_E_STEP && (!b || !c)) return PGG_ERR_ARGUMENT;
+  if (op == MIX_NEIGHBORS && k_max < 1) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_mixture_lanes<<<blocks(n, 128), 128, 0, S(stream)>>>(op, n, a, b, c, d, e, out0, out1, k_max);
+  return check_launch();
+}
+
+int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double* chol, uint64_t* states, double* sq,
+                     uint8_t* accepted, void* stream) {
+  if (n < 0 || !pi || !mu || !chol || !states || !sq || !accepted) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_sample_gauss<<<blocks(n, 128), 128, 0, S(stream)>>>(n, pi, mu, chol, states, sq, accepted);
   return check_launch();
 }
 

@@ -10,6 +10,7 @@ sampling -> training that a GPU renderer should call instead.
 behaviour, host round trip per call) or a CUDA tensor (stays resident).
 """
 
+import dataclasses
 import struct
 from dataclasses import dataclass
 from typing import NamedTuple
@@ -88,9 +89,21 @@ class RadianceSampleRec(NamedTuple):
     strategy: int
 
 
-def _wrap(stats_tensor, like, width, height, generation):
-    st = stats_tensor if torch.is_tensor(like) else stats_tensor.cpu().numpy()
-    return GuidingBuffer(width, height, st, generation)
+def _planes(g):
+    """Device planes of any GuidingBuffer-like object (ours or the
+    reference's pgtrace.guide_buffers.GuidingBuffer: width, height, stats)."""
+    return GammaPlanes.from_aos(g.stats, _conv.device())
+
+
+def _wrap(stats_tensor, like, generation):
+    """A new buffer of the caller's own GuidingBuffer class (the reference's
+    dataclass when a pgtrace session calls us), stats as NumPy or as the
+    caller's CUDA tensor type -- double buffering, generation + 1
+    (pg/guide_buffers.py:135-137, 281-283)."""
+    st = stats_tensor if torch.is_tensor(like.stats) else stats_tensor.cpu().numpy()
+    if dataclasses.is_dataclass(like):
+        return dataclasses.replace(like, stats=st, generation=generation)
+    return GuidingBuffer(like.width, like.height, st, generation)
 
 
 def reproject(gamma_prev, gbuf_prev, gbuf_cur, policy):
@@ -104,9 +117,9 @@ def reproject(gamma_prev, gbuf_prev, gbuf_cur, policy):
     cfg = PassConfig(depth_rel_tol=policy.depth_rel_tol, normal_dot_min=policy.normal_dot_min,
                      rotate_mean=policy.rotate_mean)
     miss = torch.zeros(1, dtype=torch.int32, device=dev)
-    res = run_pass(cfg, 0, cur, gamma_prev.planes(), prev=prev, height=h, want_reproj=True, want_samples=False,
+    res = run_pass(cfg, 0, cur, _planes(gamma_prev), prev=prev, height=h, want_reproj=True, want_samples=False,
                    halo_misses=miss)
-    return _wrap(res.gamma_reproj.to_aos(), gamma_prev.stats, w, h, gamma_prev.generation + 1)
+    return _wrap(res.gamma_reproj.to_aos(), gamma_prev, gamma_prev.generation + 1)
 
 
 def training_pass(gamma, vpl, gbuf, k_max=mixture.KMAX_DEFAULT, seed=0, frame_index=0,
@@ -117,9 +130,9 @@ def training_pass(gamma, vpl, gbuf, k_max=mixture.KMAX_DEFAULT, seed=0, frame_in
     dev = _conv.device()
     h, w = gamma.height, gamma.width
     cfg = PassConfig(seed=seed, k_max=k_max, neighbor_radius=neighbor_radius)
-    res = run_pass(cfg, frame_index, GBufferPlanes.from_ref(gbuf, device=dev), gamma.planes(),
+    res = run_pass(cfg, frame_index, GBufferPlanes.from_ref(gbuf, device=dev), _planes(gamma),
                    vpl=VplPlanes.from_ref(vpl, device=dev), height=h, want_samples=False)
-    return _wrap(res.gamma.to_aos(), gamma.stats, w, h, gamma.generation + 1)
+    return _wrap(res.gamma.to_aos(), gamma, gamma.generation + 1)
 
 
 def guiding_frame(gamma_prev, gbuf_prev, gbuf, vpl, seed=0, frame_index=0, spp=1, nee_draws=3,
@@ -136,7 +149,7 @@ def guiding_frame(gamma_prev, gbuf_prev, gbuf, vpl, seed=0, frame_index=0, spp=1
                      depth_rel_tol=policy.depth_rel_tol, normal_dot_min=policy.normal_dot_min,
                      rotate_mean=policy.rotate_mean, roughness_min_guide=roughness_min_guide)
     prev = GBufferPlanes.from_ref(gbuf_prev, device=dev) if gbuf_prev is not None else None
-    res = run_pass(cfg, frame_index, GBufferPlanes.from_ref(gbuf, device=dev), gamma_prev.planes(), prev=prev,
+    res = run_pass(cfg, frame_index, GBufferPlanes.from_ref(gbuf, device=dev), _planes(gamma_prev), prev=prev,
                    vpl=VplPlanes.from_ref(vpl, device=dev), height=h, want_reproj=True, want_samples=True)
     d = res.samples.dir.reshape(h * w, spp, 4)
     t = res.samples.tag.reshape(h * w, spp)
@@ -144,8 +157,8 @@ def guiding_frame(gamma_prev, gbuf_prev, gbuf, vpl, seed=0, frame_index=0, spp=1
                valid=((t >> 1) & 1).bool())
     if not torch.is_tensor(gamma_prev.stats):
         smp = {k: v.cpu().numpy() for k, v in smp.items()}
-    g_rep = _wrap(res.gamma_reproj.to_aos(), gamma_prev.stats, w, h, gamma_prev.generation + 1)
-    g_tr = _wrap(res.gamma.to_aos(), gamma_prev.stats, w, h, gamma_prev.generation + 2)
+    g_rep = _wrap(res.gamma_reproj.to_aos(), gamma_prev, gamma_prev.generation + 1)
+    g_tr = _wrap(res.gamma.to_aos(), gamma_prev, gamma_prev.generation + 2)
     return g_rep, smp, g_tr
 
 
@@ -195,7 +208,7 @@ def gather_training_batch(pixel_xy, vpl, gbuf, gamma, k_max, streams):
     h, w = gbuf.height, gbuf.width
     cur = GBufferPlanes.from_ref(gbuf, device=dev)
     vp = VplPlanes.from_ref(vpl, device=dev)
-    gp = gamma.planes()
+    gp = _planes(gamma)
     st = _conv.u64_to_dev(streams).reshape(-1)
     cfg = PassConfig(k_max=k_max, neighbor_radius=NEIGHBOR_RADIUS)
     from .layout import make_config

@@ -1,12 +1,13 @@
 """Per-pixel guiding mixture on the GPU; drop-in for pgtrace.mixture
 (pg/mixture.py).  Same names, constants, argument meaning and return types.
 
-Heavy entry points run libpgg kernels: lobe_from_stats / truncation_mass
+Every entry point runs a libpgg kernel: lobe_from_stats / truncation_mass
 (k_lobe / k_trunc: float64 covariance + reset + Cholesky, exact
-bivariate-normal truncation mass), sample_mixture (k_sample_lanes),
-m_step_update (k_m_step).  The remaining one-line densities are float64
-elementwise tensor expressions on the same device.  NumPy inputs return
-NumPy; CUDA tensors stay on the device.
+bivariate-normal truncation mass), sample_mixture (k_sample_lanes, or
+k_sample_gauss + the caller's BRDF callbacks), m_step_update (k_m_step),
+gaussian_pdf_square / mixture_pdf / box_muller / e_step_responsibility /
+neighbor_count (k_mixture_lanes, float64 in the reference's operation
+order).  NumPy inputs return NumPy; CUDA tensors stay on the device.
 """
 
 from typing import NamedTuple
@@ -86,18 +87,30 @@ def _lobe_dev(lobe):
     return GaussianLobe(*[_conv.to_dev(x, F64) for x in lobe])
 
 
+def _lanes(op, n, a, b=None, c=None, d=None, k_max=0, two=False):
+    """Run k_mixture_lanes (float64, reference operation order) on flat device arrays."""
+    dev = a.device
+    o0 = torch.empty(n, dtype=F64, device=dev)
+    o1 = torch.empty(n, dtype=F64, device=dev) if two else None
+    _lib.check(_lib.lib().pgg_mixture_lanes(op, n, _lib.ptr(a), _lib.ptr(b), _lib.ptr(c), _lib.ptr(d), None,
+                                            _lib.ptr(o0), _lib.ptr(o1), int(k_max), _lib.stream_ptr()))
+    return (o0, o1) if two else o0
+
+
+def _flat(t, lead, tail):
+    return t.expand(lead + tail).reshape((-1,) + tail).contiguous()
+
+
 def gaussian_pdf_square(lobe, p):
     """Truncated-normalised Gaussian density at square points (pg/mixture.py:158-169)."""
     torch_in = _conv.is_torch(p, *lobe)
     L = _lobe_dev(lobe)
     p = _conv.to_dev(p, F64)
-    d0 = p[..., 0] - L.mu[..., 0]
-    d1 = p[..., 1] - L.mu[..., 1]
-    l11, l21, l22 = L.chol[..., 0, 0], L.chol[..., 1, 0], L.chol[..., 1, 1]
-    z1 = d0 / l11
-    z2 = (d1 - l21 * z1) / l22
-    out = torch.exp(-0.5 * (z1 * z1 + z2 * z2)) * (1.0 / (2.0 * np.pi * l11 * l22)) / L.trunc_z
-    return _conv.back(out, torch_in)
+    lead = torch.broadcast_shapes(L.mu.shape[:-1], L.chol.shape[:-2], L.trunc_z.shape, p.shape[:-1])
+    n = int(np.prod(lead)) if lead else 1
+    out = _lanes(0, n, _flat(L.mu, lead, (2,)), _flat(L.chol, lead, (2, 2)), _flat(L.trunc_z, lead, ()),
+                 _flat(p, lead, (2,)))
+    return _conv.back(out.reshape(lead), torch_in)
 
 
 def mixture_pdf(stats, lobe, direction, brdf_pdf):
@@ -106,20 +119,33 @@ def mixture_pdf(stats, lobe, direction, brdf_pdf):
     torch_in = _conv.is_torch(stats, direction, brdf_pdf, *lobe)
     st = _conv.to_dev(stats, F64)
     sq = sgmap.hemisphere_to_square(_conv.to_dev(direction, F64))
-    g = gaussian_pdf_square(_lobe_dev(lobe), sq) / (2.0 * np.pi)
-    pi = st[..., MIX_PI]
-    out = pi * g + (1.0 - pi) * _conv.to_dev(brdf_pdf, F64)
-    return _conv.back(out, torch_in)
+    L = _lobe_dev(lobe)
+    bp = _conv.to_dev(brdf_pdf, F64)
+    lead = torch.broadcast_shapes(st.shape[:-1], L.mu.shape[:-1], L.chol.shape[:-2], L.trunc_z.shape,
+                                  sq.shape[:-1], bp.shape)
+    n = int(np.prod(lead)) if lead else 1
+    pk = torch.cat([_flat(L.mu, lead, (2,)), _flat(L.chol, lead, (2, 2)).reshape(n, 4),
+                    _flat(L.trunc_z, lead, ()).reshape(n, 1)], dim=1).contiguous()
+    out = _lanes(4, n, _flat(st[..., MIX_PI], lead, ()), pk, _flat(sq, lead, (2,)), _flat(bp, lead, ()))
+    return _conv.back(out.reshape(lead), torch_in)
 
 
 def box_muller(u1, u2):
     """Two standard normals; u1 = 0 clamps to 1e-12 (pg/mixture.py:185-190)."""
     torch_in = _conv.is_torch(u1, u2)
-    a = torch.clamp(_conv.to_dev(u1, F64), min=1e-12)
-    b = _conv.to_dev(u2, F64)
-    r = torch.sqrt(-2.0 * torch.log(a))
-    ang = 2.0 * np.pi * b
-    return _conv.back(r * torch.cos(ang), torch_in), _conv.back(r * torch.sin(ang), torch_in)
+    a, b = torch.broadcast_tensors(_conv.to_dev(u1, F64), _conv.to_dev(u2, F64))
+    lead = a.shape
+    z0, z1 = _lanes(1, a.numel(), a.contiguous().reshape(-1), b.contiguous().reshape(-1), two=True)
+    return _conv.back(z0.reshape(lead), torch_in), _conv.back(z1.reshape(lead), torch_in)
+
+
+def e_step_responsibility(pi, gauss_pdf, brdf_pdf):
+    """Posterior of the Gaussian component; 0 where both densities vanish (pg/mixture.py:262-273)."""
+    torch_in = _conv.is_torch(pi, gauss_pdf, brdf_pdf)
+    a, b, c = torch.broadcast_tensors(*(_conv.to_dev(x, F64) for x in (pi, gauss_pdf, brdf_pdf)))
+    lead = a.shape
+    out = _lanes(2, a.numel(), *(x.contiguous().reshape(-1) for x in (a, b, c)))
+    return _conv.back(out.reshape(lead), torch_in)
 
 
 class LocalBrdf(NamedTuple):
@@ -165,14 +191,24 @@ def sample_lanes(world, normal, view, kind, rough, guided, pi, lobe6, states):
 def sample_mixture(stats, lobe, brdf_sampler, brdf_pdf_fn, streams):
     """One-sample mixture draw per lane in the local frame (pg/mixture.py:193-259).
 
-    ``brdf_sampler`` is a LocalBrdf (brdf_pdf_fn is ignored: the pdf of the
-    same BRDF is evaluated on the device).  ``streams`` (uint64, one state
-    per lane) is advanced in place exactly as the reference advances it.
-    Returns (direction (n,3) local, pdf (n,), strategy uint8 (n,), valid bool (n,)).
-    """
+    Two ways to give the BRDF strategy:
+
+    * the reference's callbacks, exactly as pg/ptrace.py:201-208 passes them:
+      ``brdf_sampler(idx, sub_streams) -> (dirs (n,3) local, valid (n,))`` and
+      ``brdf_pdf_fn(idx, dirs) -> (n,)``.  The Gaussian branch (zeta draw, up
+      to 16 Box-Muller tries) runs on the device (k_sample_gauss); the
+      callbacks are then invoked on the host for exactly the lanes and
+      stream copies the reference gives them, and the mixture pdf is the
+      device's (square map + truncated Gaussian, k_sgmap / k_mixture_lanes).
+    * ``mixture.LocalBrdf(kind, roughness, wo_local)`` (brdf_pdf_fn ignored):
+      the whole draw, BRDF branch and pdf included, in one kernel
+      (k_sample_lanes) -- the fast path _sample_first_bounce uses.
+
+    ``streams`` (uint64, one state per lane) is advanced in place exactly as
+    the reference advances it.  Returns (direction (n,3) local, pdf (n,),
+    strategy uint8 (n,), valid bool (n,))."""
     if not isinstance(brdf_sampler, LocalBrdf):
-        raise TypeError("the GPU sample_mixture takes a mixture.LocalBrdf(kind, roughness, wo_local) in place of "
-                        "the reference's Python sampler/pdf callbacks (see INTEGRATION.md)")
+        return _sample_mixture_callbacks(stats, lobe, brdf_sampler, brdf_pdf_fn, streams)
     torch_in = _conv.is_torch(stats, streams)
     st = _conv.to_dev(stats, F64).reshape(-1, 8)
     n = st.shape[0]
@@ -188,15 +224,50 @@ def sample_mixture(stats, lobe, brdf_sampler, brdf_pdf_fn, streams):
     return d[:, :3], d[:, 3], (t & 1).astype(np.uint8), ((t >> 1) & 1).astype(bool)
 
 
-def e_step_responsibility(pi, gauss_pdf, brdf_pdf):
-    """Posterior of the Gaussian component; 0 where both densities vanish (pg/mixture.py:262-273)."""
-    torch_in = _conv.is_torch(pi, gauss_pdf, brdf_pdf)
-    p = _conv.to_dev(pi, F64)
-    g = p * _conv.to_dev(gauss_pdf, F64)
-    b = (1.0 - p) * _conv.to_dev(brdf_pdf, F64)
-    den = g + b
-    out = torch.where(den > 0.0, g / torch.where(den > 0.0, den, torch.ones_like(den)), torch.zeros_like(den))
-    return _conv.back(out, torch_in)
+def _sample_mixture_callbacks(stats, lobe, brdf_sampler, brdf_pdf_fn, streams):
+    """sample_mixture with the caller's BRDF callbacks (pg/mixture.py:193-259
+    step by step; the callbacks see NumPy arrays, as in the reference)."""
+    from . import sgmap
+    st = _conv.to_dev(stats, F64).reshape(-1, 8)
+    n = st.shape[0]
+    L = _lobe_dev(lobe)
+    mu = L.mu.reshape(n, 2).contiguous()
+    chol = L.chol.reshape(n, 4).contiguous()
+    pi = st[:, MIX_PI].contiguous()
+    states = _conv.u64_to_dev(streams).reshape(n).clone()
+    sq = torch.empty(n, 2, dtype=F64, device=st.device)
+    acc = torch.empty(n, dtype=torch.uint8, device=st.device)
+    _lib.check(_lib.lib().pgg_sample_gauss(n, _lib.ptr(pi), _lib.ptr(mu), _lib.ptr(chol), _lib.ptr(states),
+                                           _lib.ptr(sq), _lib.ptr(acc), _lib.stream_ptr()))
+    torch_streams = torch.is_tensor(streams)
+    host_streams = streams.cpu().numpy().view(np.uint64) if torch_streams else np.asarray(streams)
+    host_streams.reshape(n)[...] = states.cpu().numpy().view(np.uint64)
+    accepted = acc.cpu().numpy().astype(bool)
+    direction = np.zeros((n, 3))
+    if accepted.any():
+        direction[accepted] = sgmap.square_to_hemisphere(sq[torch.from_numpy(accepted).to(sq.device)].cpu().numpy())
+    brdf_lanes = np.nonzero(~accepted)[0]
+    valid = np.ones(n, dtype=bool)
+    if brdf_lanes.size:
+        hs = host_streams.reshape(n)
+        sub = hs[brdf_lanes]
+        dirs_b, ok_b = brdf_sampler(brdf_lanes, sub)
+        hs[brdf_lanes] = sub
+        direction[brdf_lanes] = dirs_b
+        valid[brdf_lanes] = ok_b
+    if torch_streams:
+        streams.view(torch.int64).copy_(torch.from_numpy(host_streams.view(np.int64)).reshape(streams.shape))
+    strategy = np.where(accepted, STRATEGY_GAUSSIAN, STRATEGY_BRDF).astype(np.uint8)
+    pdf = np.zeros(n)
+    ok_idx = np.nonzero(valid)[0]
+    if ok_idx.size:
+        b = np.asarray(brdf_pdf_fn(ok_idx, direction[ok_idx]), dtype=np.float64)
+        sel = torch.from_numpy(ok_idx).to(st.device)
+        sub_lobe = GaussianLobe(mu[sel], L.cov.reshape(n, 2, 2)[sel], L.chol.reshape(n, 2, 2)[sel],
+                                L.trunc_z.reshape(n)[sel])
+        pdf[ok_idx] = mixture_pdf(st[sel], sub_lobe, _conv.to_dev(direction[ok_idx], F64),
+                                  _conv.to_dev(b, F64)).cpu().numpy()
+    return direction, pdf, strategy, valid
 
 
 def m_step_update(stats, sq, weight, resp, valid=None, k_max=KMAX_DEFAULT):
@@ -221,6 +292,7 @@ def m_step_update(stats, sq, weight, resp, valid=None, k_max=KMAX_DEFAULT):
 def neighbor_count(k, k_max):
     """N = floor((1 - min(k,kMax)/kMax)*15 + 5 + 0.5) (pg/mixture.py:324-328)."""
     torch_in = _conv.is_torch(k)
-    kk = torch.clamp(_conv.to_dev(k, F64), max=float(k_max))
-    out = torch.floor((1.0 - kk / float(k_max)) * 15.0 + 5.0 + 0.5).to(torch.int64)
-    return _conv.back(out, torch_in)
+    kk = _conv.to_dev(k, F64)
+    lead = kk.shape
+    out = _lanes(3, kk.numel(), kk.reshape(-1).contiguous(), k_max=int(k_max)).to(torch.int64)
+    return _conv.back(out.reshape(lead), torch_in)

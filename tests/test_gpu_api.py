@@ -92,8 +92,31 @@ def test_sample_mixture_api(cuda_dev):
     assert np.abs(d - od).max() <= 1e-5
     rr = gio.rel_err(pdf, opdf)
     assert np.percentile(rr, 99.99) <= 1e-4 and rr.max() <= 1e-3
-    with pytest.raises(TypeError):
-        M.sample_mixture(st, lb, lambda i, s: None, lambda i, d: None, streams)
+    # the reference's callback form (pg/mixture.py:193-205, pg/ptrace.py:201-208):
+    # Gaussian branch on the device, the caller's BRDF sampler / pdf on the host
+    ez = np.broadcast_to(np.array([0.0, 0.0, 1.0]), (n, 3))
+    calls = []
+
+    def cb_sample(rel, sub):
+        calls.append(("sample", rel.copy()))
+        w_l, _, ok = O.brdf_draw(kind[rel], rough[rel], wo[rel], ez[rel], sub)
+        return w_l, ok
+
+    def cb_pdf(rel, dirs_l):
+        calls.append(("pdf", rel.copy()))
+        return O.brdf_density(kind[rel], rough[rel], dirs_l, wo[rel], ez[rel])
+
+    streams = O.seed_lanes(9, 1, np.arange(n), 0)
+    ref_states = streams.copy()
+    d, pdf, strat, valid = M.sample_mixture(st, lb, cb_sample, cb_pdf, streams)
+    od, opdf, ostrat, ovalid = O.draw_mixture(st, olb, kind, rough, wo, ref_states)
+    np.testing.assert_array_equal(streams, ref_states)
+    np.testing.assert_array_equal(strat, ostrat)
+    np.testing.assert_array_equal(valid, ovalid)
+    np.testing.assert_allclose(d, od, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(pdf, opdf, rtol=1e-10, atol=0)
+    assert [c[0] for c in calls] == ["sample", "pdf"]
+    np.testing.assert_array_equal(calls[0][1], np.nonzero(ostrat == 0)[0])  # exactly the reference's lanes
 
 
 def _ref_gbuf(z, prefix):
