@@ -348,6 +348,12 @@ int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double
  *       (guide_buffers.py:78-137): bit0 accepted, bit1 gates re-decided in
  *       float64, bit2 rejected by the mean rotation (z < 0), bit3 rejected by
  *       the depth / normal gates */
+/* Checked builds only (libpgg_checked.so, -DPGG_CHECKS=1: in-kernel index
+ * bounds asserts on every tile / plane access of pgg_guiding_pass): copies
+ * {failures, first site, operand a, operand b, blockIdx.x, blockIdx.y} to
+ * host memory (synchronous) and optionally resets them.  Other builds return
+ * PGG_ERR_UNSUPPORTED. */
+int pgg_debug_checks(int32_t* host_out6, int32_t reset);
 int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream);
 int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
                         int32_t* rechecks, void* stream);

@@ -178,13 +178,14 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   if (train) {
     if (kTile) {
 #if PGG_TILE_S
-      const VplTileS V{smem_u32(tile_y), (uint32_t)SL.off_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
+      const VplTileS V{smem_u32(tile_y), (uint32_t)SL.off_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols,
+                       SL.cols * SL.rows};
 #else
       const VplTile V{tile_y, tile_l, (int)(blockIdx.x * TILE_W) - R, band_y0 - R, SL.cols};
 #endif
       em_partial<kFull>(A, V, S, x, y, c_jmul, c_jadd, acc);
     } else {
-      const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
+      const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0, A.vpl.rows};
       em_partial<kFull>(A, V, S, x, y, c_jmul, c_jadd, acc);
     }
   }
@@ -195,6 +196,7 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
 #endif
   float4 o0 = g0, o1 = g1;
   if (train) m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
+  PGG_CHK(CHK_OUT, yl >= 0 && yl < A.cfg.rows && x < A.cfg.width, yl, x);
   st4(A.gout.g0, own, o0);
   st4(A.gout.g1, own, o1);
 }
@@ -974,6 +976,26 @@ int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double
   if (const int rc = device_check()) return rc;
   k_sample_gauss<<<blocks(n, 128), 128, 0, S(stream)>>>(n, pi, mu, chol, states, sq, accepted);
   return check_launch();
+}
+
+int pgg_debug_checks(int32_t* host_out6, int32_t reset) {
+#if PGG_CHECKS
+  if (!host_out6) return PGG_ERR_ARGUMENT;
+  cudaError_t e = cudaMemcpyFromSymbol(host_out6, g_pgg_check, 6 * sizeof(int32_t));
+  if (e == cudaSuccess && reset) {
+    const int32_t z[6] = {0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_pgg_check, z, sizeof(z));
+  }
+  if (e != cudaSuccess) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s", cudaGetErrorString(e));
+    return PGG_ERR_CUDA;
+  }
+  return PGG_OK;
+#else
+  (void)host_out6;
+  (void)reset;
+  return PGG_ERR_UNSUPPORTED;  // not a checked build
+#endif
 }
 
 int pgg_gamma_init(int64_t p, float* g0, float* g1, void* stream) {

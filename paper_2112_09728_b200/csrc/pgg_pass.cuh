@@ -17,6 +17,38 @@ namespace pgg {
 #define PGG_GATES_F32 1  // reprojection gates: float32 first, float64 only near the thresholds (0.5176 -> 0.5153 ms)
 #endif
 constexpr int SLOTS = 20;                 // guide_buffers.py:20
+
+// Checked builds (-DPGG_CHECKS=1, libpgg_checked.so): every shared-memory
+// tile read, global plane read and output store of the pass asserts its
+// index bounds; failures are counted (first one recorded) in device globals
+// read back by pgg_debug_checks().  compute-sanitizer is not available on
+// this pool; this is its in-kernel substitute (tests/test_gpu_checked.py).
+#ifndef PGG_CHECKS
+#define PGG_CHECKS 0
+#endif
+#if PGG_CHECKS && defined(__CUDACC__)
+__device__ int g_pgg_check[6];  // failures, first site, its two operands, blockIdx.x, blockIdx.y
+#endif
+#if PGG_CHECKS && defined(__CUDA_ARCH__)
+__device__ __noinline__ void pgg_check_fail(int site, int a, int b) {
+  if (atomicAdd(&g_pgg_check[0], 1) == 0) {
+    g_pgg_check[1] = site;
+    g_pgg_check[2] = a;
+    g_pgg_check[3] = b;
+    g_pgg_check[4] = blockIdx.x;
+    g_pgg_check[5] = blockIdx.y;
+  }
+}
+#define PGG_CHK(site, cond, a, b) \
+  do {                            \
+    if (!(cond)) pgg_check_fail(site, (int)(a), (int)(b)); \
+  } while (0)
+#else
+#define PGG_CHK(site, cond, a, b) \
+  do {                            \
+  } while (0)
+#endif
+enum : int { CHK_TILE = 1, CHK_CUR = 2, CHK_GIN = 3, CHK_PREV = 4, CHK_VPL = 5, CHK_OUT = 6, CHK_SMP = 7 };
 #ifndef PGG_PROF_TRIES
 #define PGG_PROF_TRIES 16  // measurement-only override
 #endif
@@ -176,6 +208,8 @@ PGG_HD void reproject_px(const PassArgs& A, int x, int y, uint8_t fl, const floa
   }
   const int64_t sp = (int64_t)(sy - A.prev.row0) * C.width + sx;
   const int64_t gi = (int64_t)(sy - A.gin.row0) * C.width + sx;
+  PGG_CHK(CHK_PREV, sy - A.prev.row0 >= 0 && sy - A.prev.row0 < A.prev.rows && sx >= 0 && sx < C.width, sy, sx);
+  PGG_CHK(CHK_GIN, sy - A.gin.row0 >= 0 && sy - A.gin.row0 < A.gin.rows, sy, A.gin.row0);
   // the source's gate planes and Gamma in flight together
   const uint8_t pfl = ldu8(A.prev.flags, sp);
   const float4 ndp = ld4(A.prev.nd, sp);
@@ -545,12 +579,19 @@ struct VplGlobal {
   const float* y;
   const float* L;
   int width, row0;
-  PGG_MHD float4 get_y(int cx, int cy) const { return ld4(y, (int64_t)(cy - row0) * width + cx); }
-  PGG_MHD float4 get_L(int cx, int cy) const { return ld4(L, (int64_t)(cy - row0) * width + cx); }
+  int rows;  // rows held (bounds checks of checked builds)
+  PGG_MHD float4 get_y(int cx, int cy) const { return y_at(index(cx, cy)); }
+  PGG_MHD float4 get_L(int cx, int cy) const { return L_at(index(cx, cy)); }
   PGG_MHD int64_t index(int cx, int cy) const { return (int64_t)(cy - row0) * width + cx; }
   PGG_MHD int stride() const { return width; }
-  PGG_MHD float4 y_at(int64_t i) const { return ld4(y, i); }
-  PGG_MHD float4 L_at(int64_t i) const { return ld4(L, i); }
+  PGG_MHD float4 y_at(int64_t i) const {
+    PGG_CHK(CHK_VPL, i >= 0 && i < (int64_t)rows * width, i, rows);
+    return ld4(y, i);
+  }
+  PGG_MHD float4 L_at(int64_t i) const {
+    PGG_CHK(CHK_VPL, i >= 0 && i < (int64_t)rows * width, i, rows);
+    return ld4(L, i);
+  }
 };
 struct VplTile {
   static constexpr bool kZeroOOB = true;  // TMA zero-fills tile elements outside the frame
@@ -573,6 +614,7 @@ struct VplTileS {
   uint32_t y;      // shared address of tile element (0, 0) of the y plane
   uint32_t off_l;  // byte offset of the L plane
   int x0, y0, cols;
+  int n;           // elements per plane (bounds checks of checked builds)
   PGG_MHD static float4 lds(uint32_t a) {
     float4 v;
 #ifdef __CUDA_ARCH__
@@ -585,8 +627,14 @@ struct VplTileS {
   }
   PGG_MHD int index(int cx, int cy) const { return (cy - y0) * cols + (cx - x0); }
   PGG_MHD int stride() const { return cols; }
-  PGG_MHD float4 y_at(int i) const { return lds(y + 16u * (uint32_t)i); }
-  PGG_MHD float4 L_at(int i) const { return lds(y + off_l + 16u * (uint32_t)i); }
+  PGG_MHD float4 y_at(int i) const {
+    PGG_CHK(CHK_TILE, i >= 0 && i < n, i, n);
+    return lds(y + 16u * (uint32_t)i);
+  }
+  PGG_MHD float4 L_at(int i) const {
+    PGG_CHK(CHK_TILE, i >= 0 && i < n, i, n);
+    return lds(y + off_l + 16u * (uint32_t)i);
+  }
   PGG_MHD float4 get_y(int cx, int cy) const { return y_at(index(cx, cy)); }
   PGG_MHD float4 get_L(int cx, int cy) const { return L_at(index(cx, cy)); }
 };
@@ -940,6 +988,8 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   const int y = C.row0 + yl;
   const int64_t own = (int64_t)yl * W + x;
   const int64_t ci = (int64_t)(y - A.cur.row0) * W + x;
+  PGG_CHK(CHK_CUR, y - A.cur.row0 >= 0 && y - A.cur.row0 < A.cur.rows && x >= 0 && x < W, y, x);
+  PGG_CHK(CHK_OUT, yl >= 0 && yl < C.rows, yl, C.rows);
   const uint8_t fl = ldu8(A.cur.flags, ci);
   const bool valid = fl & 1;
   // all own-pixel loads in flight together (invalid pixels are ~10 %)
@@ -955,6 +1005,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     reproject_px(A, x, y, fl, nd, pr, am, g0, g1);
   } else {
     const int64_t gi = (int64_t)(y - A.gin.row0) * W + x;
+    PGG_CHK(CHK_GIN, y - A.gin.row0 >= 0 && y - A.gin.row0 < A.gin.rows, y, A.gin.row0);
     g0 = ld4(A.gin.g0, gi);
     g1 = ld4(A.gin.g1, gi);
   }
@@ -1042,7 +1093,7 @@ PGG_HD void em_dump(const PassArgs& A, int x, int y, uint64_t s0, const uint64_t
   EmSetup S;
   em_setup(pr, va, am, (fl & 4) != 0, pf, L, g1.w, C.k_max, s0, S);
   S.n_raw = v3(nd.x, nd.y, nd.z);
-  const VplGlobal V{A.vpl.y, A.vpl.L, W, A.vpl.row0};
+  const VplGlobal V{A.vpl.y, A.vpl.L, W, A.vpl.row0, A.vpl.rows};
   for (int s = 0; s < S.nb; ++s) {
     int cx = x, cy = y;
     if (s > 0) {
@@ -1076,7 +1127,7 @@ PGG_HD void pass_pixel(const PassArgs& A, int x, int yl, const uint64_t* jmul, c
   float4 o0 = g0, o1 = g1;
   if (train) {
     float acc[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0};
+    const VplGlobal V{A.vpl.y, A.vpl.L, A.cfg.width, A.vpl.row0, A.vpl.rows};
     em_partial(A, V, S, x, A.cfg.row0 + yl, jmul, jadd, acc);
     m_step_apply(g0, g1, acc, A.cfg.k_max, o0, o1);
   }
