@@ -82,8 +82,18 @@ def _sample_first_bounce(scene, idx, pos, nrm, mat, wo, stats, lobe, guided, str
     rough = np.asarray(scene.mat_rough)[mat_np]
     n = len(idx_np)
     st = _conv.to_dev(stats, torch.float64).reshape(-1, 8)
-    if st.shape[0] != n:
-        raise ValueError("stats must hold one row per lane")
+    if st.shape[0] < n:
+        raise ValueError("stats must hold at least one row per lane of idx")
+    if st.shape[0] > n:
+        # pg/ptrace.py:288-290 passes the chunk's per-lane stats / lobe for ALL
+        # lanes while idx lists only the active ones, and pg/ptrace.py:205-213
+        # indexes them by position within idx (stats[gsel], gsel relative to
+        # idx): lane idx[j] uses row j.  With primary-ray misses that pairs a
+        # lane with another pixel's mixture; reproduced here so the drop-in
+        # returns what the reference returns (the fused pass and the GPU
+        # render use every pixel's own Gamma).
+        st = st[:n]
+        lobe = type(lobe)(*[x[:n] for x in lobe])
     if torch.is_tensor(streams):
         states = streams.view(torch.int64)[torch.as_tensor(idx_np, device=streams.device)].contiguous()
     else:

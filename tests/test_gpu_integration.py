@@ -201,3 +201,53 @@ def test_reference_callbacks_through_patched_sample_mixture(monkeypatch):
     np.testing.assert_allclose(wi1, wi0, rtol=0, atol=1e-12)
     np.testing.assert_allclose(pdf1, pdf0, rtol=1e-10, atol=0)
     assert (s0 == 1).any() and (s0 == 0).any()
+
+
+def test_first_bounce_with_primary_misses():
+    """A scene whose camera sees the background: the reference's
+    _sample_first_bounce receives the per-lane stats of ALL lanes with idx
+    listing only the hits (pg/ptrace.py:287-290) and indexes them by position
+    within idx; the drop-in reproduces that pairing -- strategies, validity
+    and streams bitwise, directions / pdfs within policy."""
+    cli, pg_gb, pg_mix, pg_pt, sc = _pgtrace()
+    from pgtrace import rng as pg_rng
+    from paper_2112_09728_b200 import ptrace as pt
+    doc = sc.BUILTIN_SCENES["cornell-occluder"]()
+    cam = dict(doc["camera"][0])
+    cam["origin"] = [1.0, 1.0, -2.5]   # behind the open front: the frame border sees the background
+    doc["camera"] = [cam]
+    scene = sc.scene_from_dict(doc)
+    w, h = 48, 32
+    gbuf = pg_pt.gbuffer_pass(scene, 0, (w, h))
+    valid = gbuf.valid.reshape(-1)
+    assert 0.05 < 1.0 - valid.mean() < 0.95
+    n = w * h
+    r = np.random.default_rng(5)
+    stats = np.tile(np.array([0.5, 0.5, 0.5, 0.5, 0.25, 0.0, 0.05, 0.0]), (n, 1))
+    stats[:, 0:2] = r.uniform(0.2, 0.8, (n, 2))
+    sd = 10 ** r.uniform(-1.5, -0.6, (n, 2))
+    stats[:, 2] = sd[:, 0] ** 2 + stats[:, 0] ** 2
+    stats[:, 3] = sd[:, 1] ** 2 + stats[:, 1] ** 2
+    stats[:, 4] = stats[:, 0] * stats[:, 1]
+    stats[:, 6] = r.uniform(0.3, 0.9, n)
+    stats[:, 7] = 3.0
+    stats = stats.astype(np.float32).astype(np.float64)
+    lobe = pg_mix.lobe_from_stats(stats)
+    idx = np.nonzero(valid)[0]
+    pos, nrm = gbuf.pos.reshape(-1, 3)[idx], gbuf.normal.reshape(-1, 3)[idx]
+    mat, wo = np.maximum(gbuf.mat.reshape(-1), 0)[idx], gbuf.view.reshape(-1, 3)[idx]
+    guided = np.ones(idx.size, dtype=bool)
+
+    def call(fn):
+        streams = pg_rng.make_streams(4, 0, np.arange(n, dtype=np.uint64))
+        out = fn(scene, idx, pos, nrm, mat, wo, stats, lobe, guided, streams)
+        return out, streams
+
+    (wi0, pdf0, s0, v0), st0 = call(pg_pt._sample_first_bounce)
+    (wi1, pdf1, s1, v1), st1 = call(pt._sample_first_bounce)
+    np.testing.assert_array_equal(st1, st0)
+    np.testing.assert_array_equal(s1, s0)
+    np.testing.assert_array_equal(v1, v0)
+    assert np.abs(wi1 - wi0).max() <= 1e-5
+    rr = gio.rel_err(pdf1[v0], pdf0[v0])
+    assert np.percentile(rr, 99.99) <= 1e-4 and rr.max() <= 1e-3
