@@ -45,6 +45,16 @@ BYTES_PER_PX = 184          # fused pass, 1 spp
 BYTES_PER_EXTRA_SPP = 17
 
 
+METRIC_1080P = "guiding-pass Mpixels/s at 1080p"
+
+
+def config_1080p(world):
+    """The config both arms print (identical dicts: same workload)."""
+    return {"workload": "1920x1080 1 spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM per frame "
+                        "(BASELINE configs[1]); N>1 = N independent streams",
+            "parallelism": "replicas" if world > 1 else "single"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -58,6 +68,10 @@ def parse():
     ap.add_argument("--no-frame-loop", action="store_true")
     ap.add_argument("--bands", action="store_true", help="row-band path even at N=1 (exercises the NCCL code)")
     ap.add_argument("--no-bands", action="store_true", help="N>1: skip the 4K 4 spp row-band leg")
+    ap.add_argument("--seq", type=int, default=0,
+                    help="time one true N-frame sequence (frames generated on the device between passes, "
+                         "not timed) instead of cycling 16 resident frames; BASELINE configs[4] is --workload 8k "
+                         "--seq 64")
     return ap.parse_args()
 
 
@@ -239,64 +253,169 @@ def cpu_host():
     return {"cpu_model": model, "host_cores": os.cpu_count()}
 
 
-def cpu_sample_rows(threads):
-    return 32 * threads
+def _pgtrace():
+    """The unmodified reference package (pip-installed from /root/reference
+    into baseline/_ref; it travels to the GPU box with the repo), or None."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "pgtrace")) and p not in sys.path:
+        sys.path.append(p)
+    try:
+        from types import SimpleNamespace
+
+        import pgtrace  # noqa: F401
+        from pgtrace import guide_buffers, mixture, ptrace, rng
+        return SimpleNamespace(gb=guide_buffers, mx=mixture, pt=ptrace, rng=rng)
+    except ImportError:
+        return None
 
 
-def run_cpu_reference(rows_per_thread=32, threads=None, frame=5, seed=0):
-    """Oracle port of the reference path on a bounded sample: `threads`
-    row bands of 1920 x rows_per_thread pixels of one 1080p frame, one band
-    per host thread (NumPy releases the GIL).  Returns (pixels, seconds, threads)."""
+_FRAMES_1080P = {}
+
+
+def frame_pair_1080p(frame=5, seed=0):
+    """Frames frame-1 and frame of the 1080p bench sequence on the host
+    (torch CPU tensors), cached."""
+    key = (frame, seed)
+    if key not in _FRAMES_1080P:
+        from paper_2112_09728_b200 import synth
+        _FRAMES_1080P.clear()
+        _FRAMES_1080P[key] = list(synth.sequence(1920, 1080, 2, seed=seed, first_frame=frame - 1))
+    return _FRAMES_1080P[key]
+
+
+def band_inputs(r0, r1, frame=5, seed=0):
+    """Rows [r0, r1) of the 1080p bench frames as a standalone frame (host
+    NumPy; float32 values as the GPU sees them), Gamma = init_stats with k
+    drawn in [0, 16) like the first 16 frames of the sequence."""
     import numpy as np
     import torch
-    from concurrent.futures import ThreadPoolExecutor
+    (gp, _), (gc, vc) = frame_pair_1080p(frame, seed)
+
+    def cut(d):
+        out = {}
+        for k, v in d.items():
+            if torch.is_tensor(v) and v.dim() >= 2 and v.shape[0] == 1080:
+                out[k] = v[r0:r1].numpy()
+            elif k == "height":
+                out[k] = r1 - r0
+            else:
+                out[k] = v.numpy() if torch.is_tensor(v) else v
+        return out
+
+    h, w = r1 - r0, 1920
+    rng = np.random.default_rng(r0)
+    st = np.tile(np.array([0.5, 0.5, 0.5, 0.5, 0.25, 0.0, 0.05, 0.0], np.float32), (h, w, 1))
+    st[..., 7] = rng.integers(0, 16, (h, w))
+    return dict(gp=cut(gp), gc=cut(gc), vc=cut(vc), gamma_in=st, frame=frame, seed=seed)
+
+
+def _ref_gbuffer(pg, d):
+    import numpy as np
+    f64 = lambda k: np.asarray(d[k], np.float64)  # noqa: E731
+    h, w = d["valid"].shape
+    return pg.pt.GBuffer(width=w, height=h, valid=np.asarray(d["valid"], bool), pos=f64("pos"), normal=f64("normal"),
+                         depth=f64("depth"), mat=np.asarray(d["mat"], np.int32), kind=np.asarray(d["kind"], np.int32),
+                         albedo=f64("albedo"), roughness=f64("roughness"), front=np.asarray(d["front"], bool),
+                         view=f64("view"), motion=f64("motion"), has_history=np.asarray(d["has_history"], bool),
+                         cam_origin=np.asarray(d["cam_origin"], np.float64))
+
+
+def reference_pass(pg, io, spp=1, nee_draws=3, reproject=True):
+    """The guiding pass through the reference's OWN functions (pgtrace):
+    guide_buffers.reproject (pg/guide_buffers.py:78-137); depth-0 sampling as
+    the render issues it (pg/ptrace.py:449-475 lane keys pixel*spp+s, the NEE
+    draws, then ptrace._sample_first_bounce, pg/ptrace.py:161-220);
+    guide_buffers.training_pass (pg/guide_buffers.py:262-283).  Returns
+    (outputs, seconds per stage)."""
+    import numpy as np
+    from types import SimpleNamespace
+    gp, gc = _ref_gbuffer(pg, io["gp"]), _ref_gbuffer(pg, io["gc"])
+    h, w = gc.height, gc.width
+    v = io["vc"]
+    vpl = pg.pt.VplBuffer(np.asarray(v["valid"], bool), np.asarray(v["y"], np.float64),
+                          np.asarray(v["radiance"], np.float64), np.asarray(v["strategy"], np.uint8))
+    seed, frame = io["seed"], io["frame"]
+    t0 = time.perf_counter()
+    g = pg.gb.GuidingBuffer(w, h, io["gamma_in"].copy())
+    if reproject:
+        g = pg.gb.reproject(g, gp, gc, pg.gb.ReprojectionPolicy())
+    t1 = time.perf_counter()
+    st = g.stats_for_render().reshape(-1, 8)
+    valid = gc.valid.reshape(-1)
+    idx = np.nonzero(valid)[0]
+    lobe = pg.mx.lobe_from_stats(st[idx])
+    kind, rough = gc.kind.reshape(-1), gc.roughness.reshape(-1)
+    guided = (valid & ((kind == 0) | (rough >= 0.05)) & (st[:, 7] >= 1.0))[idx]
+    scene = SimpleNamespace(mat_kind=kind, mat_albedo=gc.albedo.reshape(-1, 3), mat_rough=rough)
+    smp = dict(wi=np.zeros((h * w, spp, 3)), pdf=np.zeros((h * w, spp)), strategy=np.zeros((h * w, spp), np.uint8),
+               valid=np.zeros((h * w, spp), bool))
+    for s_ in range(spp):
+        streams = pg.rng.make_streams(seed, frame, np.arange(h * w, dtype=np.uint64) * np.uint64(spp) + np.uint64(s_))
+        sub = streams[idx]
+        for _ in range(nee_draws):
+            pg.rng.next_u32(sub)
+        streams[idx] = sub
+        wi, pdf, strat, ok = pg.pt._sample_first_bounce(
+            scene, idx, gc.pos.reshape(-1, 3)[idx], gc.normal.reshape(-1, 3)[idx], idx, gc.view.reshape(-1, 3)[idx],
+            st[idx], lobe, guided, streams)
+        smp["wi"][idx, s_], smp["pdf"][idx, s_], smp["strategy"][idx, s_], smp["valid"][idx, s_] = wi, pdf, strat, ok
+    t2 = time.perf_counter()
+    tr = pg.gb.training_pass(g, vpl, gc, k_max=64, seed=seed, frame_index=frame)
+    t3 = time.perf_counter()
+    out = dict(gamma_reproj=np.asarray(g.stats), samples=smp, gamma_trained=np.asarray(tr.stats))
+    return out, {"reproject": t1 - t0, "sample": t2 - t1, "train": t3 - t2}
+
+
+def oracle_pass(io, spp=1, reproject=True):
+    """The oracle port (oracle/pgg_oracle.py) of the same three stages, used
+    only when pgtrace is not importable."""
+    import numpy as np
     from types import SimpleNamespace
 
     from oracle import pgg_oracle as O
-    from paper_2112_09728_b200 import synth
-    threads = threads or (os.cpu_count() or 1)
-    h = rows_per_thread * threads
-    (gp, _), (gc, vc) = list(synth.sequence(W, h, 2, seed=seed, first_frame=frame - 1))
 
     def ns(d):
-        return SimpleNamespace(**{k: (v.numpy().astype(np.float64) if torch.is_tensor(v) and v.dtype == torch.float32
-                                      else (v.numpy() if torch.is_tensor(v) else v)) for k, v in d.items()})
+        return SimpleNamespace(**{k: (np.asarray(v, np.float64) if isinstance(v, np.ndarray) and v.dtype == np.float32
+                                      else v) for k, v in d.items()})
+    gp, gc, vc = ns(io["gp"]), ns(io["gc"]), ns(io["vc"])
+    t0 = time.perf_counter()
+    g = O.reproject(io["gamma_in"], gp, gc) if reproject else io["gamma_in"]
+    t1 = time.perf_counter()
+    smp = O.sample_frame(g, gc, io["seed"], io["frame"], spp=spp)
+    t2 = time.perf_counter()
+    tr = O.train(g, vc, gc, seed=io["seed"], frame=io["frame"])
+    t3 = time.perf_counter()
+    return (dict(gamma_reproj=g, samples=smp, gamma_trained=tr),
+            {"reproject": t1 - t0, "sample": t2 - t1, "train": t3 - t2})
 
-    gpn, gcn, vcn = ns(gp), ns(gc), ns(vc)
-    rng = np.random.default_rng(0)
-    st = O.fresh_stats(h * W).reshape(h, W, 8).astype(np.float32)
-    st[..., 7] = rng.integers(0, 16, (h, W))
 
-    def cut(n, r0, r1):
-        return SimpleNamespace(**{k: (v[r0:r1] if isinstance(v, np.ndarray) and v.ndim >= 2 and v.shape[0] == h
-                                      else v) for k, v in vars(n).items()})
+def run_cpu_reference(rows_per_thread=32, threads=None, frame=5, seed=0):
+    """The reference CPU path on a bounded sample of the 1080p workload:
+    `threads` row bands of 1920 x rows_per_thread pixels spread evenly over
+    frame `frame` of the bench sequence, each run as a standalone frame, one
+    band per host thread (NumPy releases the GIL).  pgtrace itself when it
+    is importable (kind "reference"), else the oracle port ("port").
+    Returns (pixels, seconds, threads, kind)."""
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or (os.cpu_count() or 1)
+    pg = _pgtrace()
+    kind = "reference" if pg is not None else "port"
+    step = 1080 // threads
+    bands = [(i * step + (step - rows_per_thread) // 2, i * step + (step - rows_per_thread) // 2 + rows_per_thread)
+             for i in range(threads)]
+    inputs = [band_inputs(r0, r1, frame, seed) for r0, r1 in bands]
 
-    stages = {"reproject": 0.0, "sample": 0.0, "train": 0.0}
-
-    def band(i):
-        r0, r1 = i * rows_per_thread, (i + 1) * rows_per_thread
-        gp_, gc_, vc_ = cut(gpn, r0, r1), cut(gcn, r0, r1), cut(vcn, r0, r1)
-        t0 = time.perf_counter()
-        g = O.reproject(st[r0:r1], gp_, gc_)           # guide_buffers.reproject
-        t1 = time.perf_counter()
-        smp = O.sample_frame(g, gc_, seed, frame)        # lobe_from_stats + _sample_first_bounce
-        t2 = time.perf_counter()
-        tr = O.train(g, vc_, gc_, seed=seed, frame=frame)  # training_pass
-        t3 = time.perf_counter()
-        if threads == 1:
-            stages["reproject"] += t1 - t0
-            stages["sample"] += t2 - t1
-            stages["train"] += t3 - t2
-            # inputs and outputs of the timed sample, for the in-bench parity check
-            run_cpu_reference.last_io = dict(gp=gp, gc=gc, vc=vc, gamma_in=st, frame=frame, seed=seed,
-                                             gamma_reproj=g, samples=smp, gamma_trained=tr)
+    def band(io):
+        return reference_pass(pg, io) if pg is not None else oracle_pass(io)
 
     t = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
-        list(ex.map(band, range(threads)))
+        res = list(ex.map(band, inputs))
+    secs = time.perf_counter() - t
     if threads == 1:
-        run_cpu_reference.last_stages = {k: round(v, 3) for k, v in stages.items()}
-    return W * h, time.perf_counter() - t, threads
+        run_cpu_reference.last_stages = {k: round(v, 3) for k, v in res[0][1].items()}
+        run_cpu_reference.last_io = dict(inputs[0], **res[0][0], rows=bands[0])
+    return 1920 * rows_per_thread * threads, secs, threads, kind
 
 
 def parity_vs_cpu(dev):
@@ -331,7 +450,9 @@ def parity_vs_cpu(dev):
     smp = io["samples"]
     ok = smp["valid"][:, 0] & ((t >> 1) & 1).astype(bool)
     pr = rel(d[ok, 3], smp["pdf"][ok, 0])
-    return {"sample": f"the cpu_baseline input ({got.shape[1]}x{got.shape[0]}, random k in [0, 16))",
+    return {"sample": f"the cpu_baseline input: rows {io['rows'][0]}-{io['rows'][1] - 1} of frame {io['frame']} of the "
+                      f"1080p sequence as a standalone {got.shape[1]}x{got.shape[0]} frame, k in [0, 16)",
+            "against": "pgtrace (the reference itself, baseline/_ref)" if _pgtrace() is not None else "oracle port",
             "gamma_rel_p9999": float(np.percentile(g, 99.99)), "gamma_rel_max": float(g.max()),
             "gamma_reproj_rel_max": float(rep.max()),
             "k_equal": bool(np.array_equal(got[..., 7], ref[..., 7])),
@@ -344,27 +465,34 @@ def parity_vs_cpu(dev):
 
 
 def bench_reference(args, rank, world):
+    """--impl reference: the reference's own CPU path (pgtrace from
+    baseline/_ref; the oracle port only if it is missing) on all host cores,
+    rank 0 only, same metric / unit / config as our arm."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
+    rows = 8
+    kind = "reference"
     for _ in range(max(args.warmup, 0)):
-        run_cpu_reference(rows_per_thread=8, threads=threads)
+        run_cpu_reference(rows_per_thread=rows, threads=threads)
     px = secs = 0.0
     for _ in range(args.steps):
-        p, s, _ = run_cpu_reference(rows_per_thread=8, threads=threads)
+        p, s_, _, kind = run_cpu_reference(rows_per_thread=rows, threads=threads)
         px += p
-        secs += s
+        secs += s_
     mpix = px / secs / 1e6
-    sample = f"{threads} row bands of 1920x8 px of a 1080p frame per step (one band per host thread)"
-    line = {"impl": "reference", "metric": "guiding-pass Mpixels/s at 1080p", "value": mpix, "unit": "Mpixels/s",
+    impl = ("pgtrace (the reference package itself, pip-installed from /root/reference into baseline/_ref): "
+            "guide_buffers.reproject, ptrace._sample_first_bounce with the render's lane setup, "
+            "guide_buffers.training_pass" if kind == "reference" else "CPU oracle port of pgtrace (oracle/pgg_oracle.py)")
+    sample = (f"{threads} row bands of 1920x{rows} px spread over frame 5 of the 1080p sequence, each a standalone "
+              f"frame, one band per host thread")
+    line = {"impl": "reference", "metric": METRIC_1080P, "value": mpix, "unit": "Mpixels/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / args.steps, "ms_per_1080p_frame": 1e3 * W * H / (mpix * 1e6),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "1920x1080 1 spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM "
-                                   "per frame (BASELINE configs[1]); N>1 = N independent streams",
-                       "implementation": "CPU oracle port of pgtrace (reproject, depth-0 sampling, training_pass)",
-                       "sample": sample},
-            "cpu_baseline": {"value": mpix, "unit": "Mpixels/s", "cores": threads, "kind": "port", "sample": sample},
+            "config": config_1080p(world), "implementation": impl, "sample": sample,
+            "cpu_baseline": {"value": mpix, "unit": "Mpixels/s", "cores": threads, "kind": kind, "sample": sample,
+                             **cpu_host()},
             "e2e": {"value": mpix, "unit": "Mpixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -522,25 +650,30 @@ def bench_ours(args, rank, world, local_rank):
         bands = bench_bands(args, rank, world, local_rank, w4, h4, spp4, max(8, min(args.steps, 32)),
                             max(3, args.warmup), "4k4spp")
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        px, secs, thr = run_cpu_reference(rows_per_thread=216, threads=1)
-        cpu = {"value": px / secs / 1e6, "unit": "Mpixels/s", "cores": thr, "kind": "port",
-               "sample": f"one 1920x216 band of a 1080p frame ({px} px, {secs:.1f} s): reproject + depth-0 "
-                         f"sampling + training_pass, oracle port of pgtrace on 1 core",
+    c0 = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "1080p":
+        px, secs, thr, kind = run_cpu_reference(rows_per_thread=216, threads=1)
+        cpu = {"value": px / secs / 1e6, "unit": "Mpixels/s", "cores": thr, "kind": kind,
+               "sample": f"rows 432-647 of frame 5 of the 1080p sequence as a standalone 1920x216 frame ({px} px, "
+                         f"{secs:.1f} s): reproject + depth-0 sampling + training_pass on 1 core, "
+                         + ("pgtrace itself (baseline/_ref)" if kind == "reference" else "oracle port of pgtrace"),
                "stage_seconds": getattr(run_cpu_reference, "last_stages", None), **cpu_host()}
         cpu["parity"] = parity_vs_cpu(dev)
+        c0 = bench_config0(dev)
     if rank == 0:
-        metric = ("guiding-pass Mpixels/s at 1080p" if args.workload == "1080p"
+        metric = (METRIC_1080P if args.workload == "1080p"
                   else f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp)")
         line = {"metric": metric, "value": mpix, "unit": "Mpixels/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_frame": ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic",
-                "config": {"workload": "%dx%d %d spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM "
-                                       "per frame (BASELINE %s); N>1 = N independent streams"
-                                       % (W, H, args.spp, WORKLOADS[args.workload][3].split(":")[0]),
-                           "l2": "inputs larger than L2 (~200 MB/frame, 16 frames rotating); no flush",
-                           "parallelism": "replicas" if world > 1 else "single", **wstats},
+                "config": (config_1080p(world) if args.workload == "1080p" else
+                           {"workload": "%dx%d %d spp 16-frame synthetic sequence, fused reproject+sample/pdf(MIS)+EM "
+                                        "per frame (BASELINE %s)" % (W, H, args.spp,
+                                                                     WORKLOADS[args.workload][3].split(":")[0]),
+                            "parallelism": "replicas" if world > 1 else "single"}),
+                "l2": "inputs larger than L2 (~200 MB/frame, 16 frames rotating); no flush",
+                "workload_stats": wstats,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": ncu_traffic(args.workload), "peak_kind": peak_kind,
                              "algorithmic_bytes_per_px": bpx, "kernel_ms": kavg,
@@ -549,9 +682,130 @@ def bench_ours(args, rank, world, local_rank):
                 "clocks": clk.summary(),
                 "gpu_launches": gpu_launches,
                 "e2e": e2e, "cpu_baseline": cpu, "frame_loop": floop}
+        if c0 is not None:
+            line["config0_256"] = c0
         if bands is not None:
             line["bands_4k4spp"] = bands
         print(json.dumps(line), flush=True)
+
+
+def bench_config0(dev, reps=200):
+    """BASELINE configs[0]: a 256x256 synthetic G-buffer + 1 spp radiance
+    samples, single-frame EM update and guided sampling -- the GPU pass and
+    the reference CPU path (pgtrace, 1 core) on the same frame in the same
+    run, with the parity of the two."""
+    import numpy as np
+    import torch
+
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.layout import GammaPlanes, GBufferPlanes, PassConfig, VplPlanes
+    from paper_2112_09728_b200.session import run_pass
+    (gp, _), (gc, vc) = list(synth.sequence(256, 256, 2, seed=0, first_frame=4))
+    rng = np.random.default_rng(7)
+    st = np.tile(np.array([0.5, 0.5, 0.5, 0.5, 0.25, 0.0, 0.05, 0.0], np.float32), (256, 256, 1))
+    st[..., 7] = rng.integers(0, 16, (256, 256))
+    npd = lambda d: {k: (v.numpy() if torch.is_tensor(v) else v) for k, v in d.items()}  # noqa: E731
+    io = dict(gp=npd(gp), gc=npd(gc), vc=npd(vc), gamma_in=st, frame=5, seed=0)
+    cur = GBufferPlanes.from_ref(gc, device=dev)
+    vpl = VplPlanes.from_ref(vc, device=dev)
+    gin = GammaPlanes.from_aos(st, dev)
+    cfg = PassConfig(seed=0, spp=1)
+    out = GammaPlanes.empty(256, 256, dev)
+    for _ in range(10):
+        r = run_pass(cfg, 5, cur, gin, vpl=vpl, out_gamma=out)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        r = run_pass(cfg, 5, cur, gin, vpl=vpl, out_gamma=out, out_samples=r.samples)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    gpu_ms = e0.elapsed_time(e1) / reps
+    pg = _pgtrace()
+    if pg is not None:
+        t = time.perf_counter()
+        ref, stages = reference_pass(pg, io, reproject=False)
+        cpu_s = time.perf_counter() - t
+        kind = "reference"
+    else:
+        t = time.perf_counter()
+        ref, stages = oracle_pass(io, reproject=False)
+        cpu_s = time.perf_counter() - t
+        kind = "port"
+    got = r.gamma.to_aos().cpu().numpy()
+    rel = np.abs(got.astype(np.float64) - ref["gamma_trained"]) / np.maximum(np.abs(ref["gamma_trained"]), 1e-7)
+    t_ = r.samples.tag.cpu().numpy().reshape(-1)
+    d = r.samples.dir.cpu().numpy().reshape(-1, 4)
+    return {"workload": "BASELINE configs[0]: 256x256 synthetic G-buffer + 1 spp VPLs, one EM update + guided "
+                        "depth-0 sampling (no reprojection), k in [0, 16)",
+            "gpu_ms_per_frame": gpu_ms, "gpu_Mpixels_per_s": 65536 / (gpu_ms * 1e-3) / 1e6,
+            "gpu_timing": f"CUDA events over {reps} back-to-back launches (inputs 6 MB: L2-resident)",
+            "cpu_ms_per_frame": 1e3 * cpu_s, "cpu_Mpixels_per_s": 65536 / cpu_s / 1e6, "cpu_kind": kind,
+            "cpu_cores": 1, "cpu_stage_seconds": {k: round(v, 3) for k, v in stages.items()},
+            "gpu_vs_cpu": cpu_s * 1e3 / gpu_ms,
+            "parity": {"gamma_rel_p9999": float(np.percentile(rel, 99.99)), "gamma_rel_max": float(rel.max()),
+                       "k_equal": bool(np.array_equal(got[..., 7], ref["gamma_trained"][..., 7])),
+                       "tags_equal": bool(np.array_equal(t_ & 1, ref["samples"]["strategy"][:, 0]) and
+                                          np.array_equal(((t_ >> 1) & 1).astype(bool), ref["samples"]["valid"][:, 0])),
+                       "dir_abs_max": float(np.abs(d[:, :3] - ref["samples"]["wi"][:, 0]).max())}}
+
+
+def bench_sequence(args, rank, world, local_rank):
+    """BASELINE configs[4]: one true `--seq`-frame sequence (64 at 8K):
+    Gamma carried through every frame (k grows to 63, the EM budget shrinks
+    from 20 to 5 candidates as in a long run), each frame's inputs generated
+    on the device just before its pass (not timed), every pass timed with
+    CUDA events on its stream; ms/frame = mean over the sequence, max over
+    ranks (N > 1: N independent sequences, weak scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.layout import GBufferPlanes, PassConfig, VplPlanes
+    from paper_2112_09728_b200.session import GuidingSession
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    sess = GuidingSession(W, H, PassConfig(seed=rank, spp=args.spp), device=dev)
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    with ClockSampler(local_rank) as clk:
+        clk.wait_ready()
+        h0 = time.monotonic()
+        for f, (g, v) in enumerate(synth.sequence(W, H, args.seq, seed=rank, device=dev)):
+            gb, vp = GBufferPlanes.from_ref(g, device=dev), VplPlanes.from_ref(v, device=dev)
+            del g, v
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sess.step(gb, vp, f)
+            b.record(stream)
+            b.synchronize()
+            times.append(a.elapsed_time(b))
+        clk.mark(h0, time.monotonic())
+    ms = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    bpx = BYTES_PER_PX + BYTES_PER_EXTRA_SPP * (args.spp - 1)
+    line = {"metric": f"guiding-pass Mpixels/s ({W}x{H}, {args.spp} spp, {args.seq}-frame sequence)",
+            "value": world * W * H / (ms * 1e-3) / 1e6, "unit": "Mpixels/s", "n_gpus": world, "steps": args.seq,
+            "warmup": 0, "ms_per_step": ms, "ms_per_frame": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{WORKLOADS[args.workload][3]}, one {args.seq}-frame sequence",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "l2": "inputs larger than L2 (one frame is > 3 GB at 8K); no flush",
+            "timing": "CUDA events around each fused pass; input generation between passes not timed",
+            "ms_first_last_frames": [round(times[0], 4), round(times[-1], 4)],
+            "ms_min_max": [round(min(times), 4), round(max(times), 4)],
+            "roofline": {"bound": "hbm", "achieved": bpx * W * H / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": bpx * W * H / (ms * 1e-3) / 1e9 / peak, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_px": bpx},
+            "clocks": clk.summary(), "gpu_launches": args.seq, "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
 
 
 def bench_frame_loop(dev, frames=16, warmup=4):
@@ -712,7 +966,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
     __graft_entry__.build()
-    if args.bands or (world > 1 and args.workload != "1080p"):
+    if args.seq:
+        bench_sequence(args, rank, world, local_rank)
+    elif args.bands or (world > 1 and args.workload != "1080p"):
         line = bench_bands(args, rank, world, local_rank, W, H, args.spp, args.steps, args.warmup, args.workload)
         if line is not None:
             print(json.dumps(line), flush=True)
