@@ -46,7 +46,7 @@ constexpr int TILE_W = 32, TILE_H = PGG_TILE_H, THREADS = TILE_W * TILE_H;
 constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this radius
 
 #ifndef PGG_PHASE_SYNC
-#define PGG_PHASE_SYNC 1  // block-wide barrier between stage 1 and the EM loop: 0.5585 vs 0.5623 ms
+#define PGG_PHASE_SYNC 0  // block-wide barrier between stage 1 and the EM loop: helped in round 1 (0.5585 vs 0.5623 ms), costs 0.4 % now (0.4642 vs 0.4624 ms)
 #endif
 #ifndef PGG_TILE_S
 #define PGG_TILE_S 1

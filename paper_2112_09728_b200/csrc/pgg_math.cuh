@@ -616,11 +616,59 @@ struct PixelFrame {
   bool co_pos;      // wo . n > 0 (reference float64 sum order, stored n)
   float om_nn;      // 1 - |n|^2 of the stored normal (kept relative-exact)
 };
+// Fast float64 reciprocal / reciprocal square root for values that are
+// rounded to float32 afterwards: MUFU seed (rcp / rsqrt .approx.f64, ~2^-23)
+// and two Newton steps (~1 ulp of float64) instead of the correctly rounded
+// division / sqrt sequences with their slow-path branches.
+#ifndef PGG_FAST_F64
+#define PGG_FAST_F64 1
+#endif
+PGG_HD double d_rcp(double x) {
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+PGG_HD double d_rsqrt(double x) {
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return fma(y, fma(-h * y, y, 0.5), y);
+#else
+  return 1.0 / sqrt(x);
+#endif
+}
+
+template <class T> PGG_HD Frame<T> make_frame_fast(const V3<T>& n) {
+  const T s = m_copysign(T(1), n.z);
+  const T a = -d_rcp(s + n.z);
+  const T b = n.x * n.y * a;
+  Frame<T> f;
+  f.t = {T(1) + s * n.x * n.x * a, s * b, -s * n.x};
+  f.b = {b, s + n.y * n.y * a, -n.y};
+  f.n = n;
+  return f;
+}
+
 PGG_HD PixelFrame make_pixel_frame(const V3<float>& n, const V3<float>& wo) {
   const V3<double> nd = cvt<double>(n);
   const double nn = dot(nd, nd);
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  const V3<double> nh = nd * d_rsqrt(fmax(nn, 1e-300));
+  const Frame<double> fd = make_frame_fast(nh);
+#else
   const V3<double> nh = nd * (1.0 / sqrt(fmax(nn, 1e-300)));
   const Frame<double> fd = make_frame(nh);
+#endif
   const V3<double> wd = cvt<double>(wo);
   PixelFrame p;
   p.fr.t = cvt<float>(fd.t);
@@ -1016,16 +1064,32 @@ PGG_HD LobeF make_lobe(float mxf, float myf, float m2xx, float m2yy, float m2xy,
   const double q = radd(rmul(0.25, rmul(dd, dd)), rmul(sxy, sxy));
   // zero operands (reset and fresh lobes: sxy = 0) would take the slow
   // paths of the float64 sqrt / division; the results are the same values
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  // the reset DECISION keeps the correctly rounded sqrt of the reference
+  // within a few float64 ulps of the threshold; the Cholesky factors are
+  // rounded to float32 and take the fast reciprocals
+  double delta = q > 0.0 ? q * d_rsqrt(q) : 0.0;
+  if (fabs(rsub(half, delta) - 1e-6) <= 1e-15 * (half + delta + 1e-6)) delta = sqrt(q);
+#else
   const double delta = q > 0.0 ? sqrt(q) : 0.0;
+#endif
   const bool reset = rsub(half, delta) < 1e-6;
   if (reset) {
     sxx = 0.05;
     syy = 0.05;
     sxy = 0.0;
   }
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  const double ri11 = d_rsqrt(sxx);
+  const double l11 = sxx * ri11;
+  const double l21 = sxy == 0.0 ? sxy : sxy * ri11;
+  const double v22 = fmax(rsub(syy, rmul(l21, l21)), 1e-30);
+  const double l22 = v22 * d_rsqrt(v22);
+#else
   const double l11 = sqrt(sxx);
   const double l21 = sxy == 0.0 ? sxy : sxy / l11;
   const double l22 = sqrt(fmax(rsub(syy, rmul(l21, l21)), 1e-30));
+#endif
   LobeF L;
   L.mx = mxf;
   L.my = myf;

@@ -13,6 +13,9 @@
 
 namespace pgg {
 
+#ifndef PGG_SHARE_LANE_HASH
+#define PGG_SHARE_LANE_HASH 1
+#endif
 #ifndef PGG_GATES_F32
 #define PGG_GATES_F32 1  // reprojection gates: float32 first, float64 only near the thresholds (0.5176 -> 0.5153 ms)
 #endif
@@ -158,6 +161,79 @@ PGG_HD void lobe_chol_d(float mxf, float myf, float m2xx, float m2yy, float m2xy
 // ---------------------------------------------------------------------------
 // reprojection of one pixel (guide_buffers.py:78-137)
 
+// sin(pi t), cos(pi t) for |t| <= 1/4: Taylor series in x = pi t to x^17 /
+// x^18 (truncation < 1e-19 on |x| <= pi/4)
+PGG_HD void sincospi_quarter(double t, double& s, double& c) {
+  const double x = 3.141592653589793 * t;
+  const double u = x * x;
+  double ps = 2.8114572543455206e-15;             // 1/17!
+  ps = fma(ps, u, -7.647163731819816e-13);        // -1/15!
+  ps = fma(ps, u, 1.6059043836821613e-10);        // 1/13!
+  ps = fma(ps, u, -2.505210838544172e-08);        // -1/11!
+  ps = fma(ps, u, 2.7557319223985893e-06);        // 1/9!
+  ps = fma(ps, u, -0.0001984126984126984);        // -1/7!
+  ps = fma(ps, u, 0.008333333333333333);          // 1/5!
+  ps = fma(ps, u, -0.16666666666666666);          // -1/3!
+  s = fma(ps * u, x, x);
+  double pc = -1.5619206968586225e-16;            // -1/18!
+  pc = fma(pc, u, 4.779477332387385e-14);         // 1/16!
+  pc = fma(pc, u, -1.1470745597729725e-11);       // -1/14!
+  pc = fma(pc, u, 2.08767569878681e-09);          // 1/12!
+  pc = fma(pc, u, -2.755731922398589e-07);        // -1/10!
+  pc = fma(pc, u, 2.48015873015873e-05);          // 1/8!
+  pc = fma(pc, u, -0.001388888888888889);         // -1/6!
+  pc = fma(pc, u, 0.041666666666666664);          // 1/4!
+  pc = fma(pc, u, -0.5);                          // -1/2!
+  c = fma(pc, u, 1.0);
+}
+
+// sq_to_dir<double> (sgmap.py:21-33, 59-65) with the concentric angle
+// reduced to |t| <= 1/4 (the else-branch angle pi (1/2 - t) swaps sin/cos)
+PGG_HD V3<double> sq_to_dir_f64(float px, float py) {
+  const double a = 2.0 * (double)px - 1.0;
+  const double b = 2.0 * (double)py - 1.0;
+  double r, s, c;
+  if (fabs(a) > fabs(b)) {
+    r = a;
+    sincospi_quarter(0.25 * (b * d_rcp(a)), s, c);
+  } else if (b != 0.0) {
+    r = b;
+    sincospi_quarter(0.25 * (a * d_rcp(b)), c, s);  // sin(pi/2 - x) = cos x
+  } else {
+    r = 0.0;
+    s = 0.0;
+    c = 1.0;
+  }
+  const double r2 = r * r;
+  const double l2 = fmax(2.0 - r2, 0.0);
+  const double lift = l2 > 0.0 ? l2 * d_rsqrt(l2) : 0.0;
+  return {r * c * lift, r * s * lift, 1.0 - r2};
+}
+
+// dir_to_sq<double> (sgmap.py:67-77, 41-56) on the fast reciprocals
+PGG_HD void dir_to_sq_f64(const V3<double>& v, double& sx, double& sy) {
+  const double is = d_rsqrt(fmax(1.0 + v.z, 1e-30));
+  const double x = v.x * is;
+  const double y = v.y * is;
+  const double r2 = x * x + y * y;
+  double a, b;
+  if (r2 == 0.0) {
+    a = 0.0;
+    b = 0.0;
+  } else {
+    const double rho = r2 * d_rsqrt(r2);
+    if (fabs(x) >= fabs(y)) {
+      a = copysign(rho, x);
+      b = atan(y * d_rcp(x)) * (4.0 * K<double>::inv_pi) * a;
+    } else {
+      b = copysign(rho, y);
+      a = atan(x * d_rcp(y)) * (4.0 * K<double>::inv_pi) * b;
+    }
+  }
+  sx = fmin(fmax((a + 1.0) * 0.5, 0.0), 1.0);
+  sy = fmin(fmax((b + 1.0) * 0.5, 0.0), 1.0);
+}
+
 // Mean rotation between the previous and current tangent frames
 // (guide_buffers.py:117-133), in float64: M2 is carried unrotated, so the
 // covariance M2 - mu mu^T of the next lobe cancels and amplifies any error
@@ -173,14 +249,26 @@ PGG_COLD void rotate_or_reject(const V3<float>& np_, const V3<float>& nc, float 
   if (np_.x == nc.x && np_.y == nc.y && np_.z == nc.z && mux >= 1e-6f && mux <= 1.0f - 1e-6f &&
       muy >= 1e-6f && muy <= 1.0f - 1e-6f)
     return;
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  // float64 throughout, with range-reduced polynomials and Newton-refined
+  // MUFU seeds instead of the library's general sincospi / division / sqrt
+  // (~1 ulp of float64; the result is rounded to float32)
+  const V3<double> dl = sq_to_dir_f64(mux, muy);
+  V3<double> dc = make_frame_fast(cvt<double>(nc)).to_local(make_frame_fast(cvt<double>(np_)).to_world(dl));
+#else
   const V3<double> dl = sq_to_dir<double>((double)mux, (double)muy);
   V3<double> dc = make_frame(cvt<double>(nc)).to_local(make_frame(cvt<double>(np_)).to_world(dl));
+#endif
   if (dc.z < 0.0) {
     keep = false;
     return;
   }
   double sx, sy;
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  dir_to_sq_f64(dc, sx, sy);
+#else
   dir_to_sq<double>(dc, sx, sy);
+#endif
   ox = (float)sx;
   oy = (float)sy;
 }
@@ -930,16 +1018,27 @@ PGG_HD void m_step_apply(const float4& g0, const float4& g1, const float* acc, i
   const float sw = acc[0], swr = acc[1];
   if (!(sw > 0.0f)) return;  // no information: unchanged, k unchanged
   const double k = g1.w;
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  // reciprocals to ~1 ulp of float64; the results are rounded to float32
+  const double eta = d_rcp(fmin(k + 1.0, (double)kmax));  // = max(1/(k+1), 1/kMax)
+  const double om1 = 1.0 - eta;
+  const double ed = eta * d_rcp(fmax((double)swr, 1e-8));
+#else
   const double eta = 1.0 / fmin(k + 1.0, (double)kmax);  // = max(1/(k+1), 1/kMax): division is monotone
   const double om1 = 1.0 - eta;
   const double ed = eta / fmax((double)swr, 1e-8);
+#endif
   o0.x = (float)(om1 * g0.x + ed * (double)acc[2]);
   o0.y = (float)(om1 * g0.y + ed * (double)acc[3]);
   o0.z = (float)(om1 * g0.z + ed * (double)acc[4]);
   o0.w = (float)(om1 * g0.w + ed * (double)acc[5]);
   o1.x = (float)(om1 * g1.x + ed * (double)acc[6]);
   o1.y = (float)(om1 * g1.y + eta * (double)swr);
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  const double pit = (double)swr * d_rcp(fmax((double)sw, 1e-8));
+#else
   const double pit = (double)swr / fmax((double)sw, 1e-8);
+#endif
   o1.z = (float)fmin(fmax(om1 * g1.z + eta * pit, 0.05), 0.95);
   o1.w = (float)(k + 1.0);
 }
@@ -1032,6 +1131,9 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   const bool glossy = (fl & 4) != 0;
   const PixelFrame pf = make_pixel_frame(n, wo);
   const uint64_t pix = (uint64_t)y * (uint64_t)W + (uint64_t)x;
+#if PGG_SHARE_LANE_HASH
+  const uint64_t hpix = splitmix64(pix);  // rng.make_streams' lane hash, shared by both streams
+#endif
 #ifdef PGG_PROF_NO_SMP
   if (false) {  // measurement-only build
 #else
@@ -1050,7 +1152,14 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     cd.m2xy = g1.x;
     cd.from_floats = 0;
     for (int s = 0; s < C.spp; ++s) {
+#if PGG_SHARE_LANE_HASH
+      // spp == 1: the sampling lane key equals the pixel key of the EM stream
+      uint64_t st = (C.spp == 1 ? splitmix64(C.key_sample ^ hpix)
+                                : splitmix64(C.key_sample ^ splitmix64(pix * (uint64_t)C.spp + (uint64_t)s))) *
+                        PCG_MUL + PCG_INC;
+#else
       uint64_t st = pcg_lane(C.key_sample, pix * (uint64_t)C.spp + (uint64_t)s);
+#endif
       if (C.nee_draws == 3) {
         st = st * J3_MUL + J3_ADD;  // the three NEE draws as one jump
       } else {
@@ -1062,7 +1171,11 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
     }
   }
   if (!A.has_vpl) return false;
+#if PGG_SHARE_LANE_HASH
+  em_setup(pr, va, am, glossy, pf, L, g1.w, C.k_max, splitmix64(C.key_train ^ hpix) * PCG_MUL + PCG_INC, S);
+#else
   em_setup(pr, va, am, glossy, pf, L, g1.w, C.k_max, pcg_lane(C.key_train, pix), S);
+#endif
   S.n_raw = n;
   // view below the surface: every record has f = 0, so the batch carries no
   // weight and the reference leaves Gamma (and k) unchanged -- skip the EM
