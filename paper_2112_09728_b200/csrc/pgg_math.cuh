@@ -314,9 +314,34 @@ PGG_HD uint64_t pcg_lane(uint64_t key, uint64_t lane) {
   return splitmix64(key ^ splitmix64(lane)) * PCG_MUL + PCG_INC;
 }
 
+// One LCG step s * PCG_MUL + PCG_INC (mod 2^64).  On the device the
+// increment is added with carry-chained immediates (IADD3 / IADD3.X) instead
+// of the 64-bit addend of IMAD.WIDE, which ptxas rematerialises into a
+// register pair (two MOVs) on every step of the record loop.
+#ifndef PGG_LCG_IMM
+#define PGG_LCG_IMM 1
+#endif
+PGG_HD uint64_t lcg_step(uint64_t s) {
+#if defined(__CUDA_ARCH__) && PGG_LCG_IMM
+  uint64_t r;
+  asm("{\n\t.reg .u64 m;\n\t.reg .u32 lo, hi;\n\t"
+      "mul.lo.u64 m, %1, 6364136223846793005;\n\t"
+      "mov.b64 {lo, hi}, m;\n\t"
+      "add.cc.u32 lo, lo, 4150755663;\n\t"
+      "addc.u32 hi, hi, 335903614;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r)
+      : "l"(s));
+  return r;
+#else
+  return s * PCG_MUL + PCG_INC;
+#endif
+}
+static_assert((PCG_INC & 0xFFFFFFFFull) == 4150755663ull && (PCG_INC >> 32) == 335903614ull, "PCG increment halves");
+
 PGG_HD uint32_t pcg_next(uint64_t& s) {
   const uint64_t old = s;
-  s = old * PCG_MUL + PCG_INC;
+  s = lcg_step(old);
   const uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
   const uint32_t rot = (uint32_t)(old >> 59);
   return (xs >> rot) | (xs << ((32u - rot) & 31u));

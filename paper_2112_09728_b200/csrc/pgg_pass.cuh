@@ -13,6 +13,9 @@
 
 namespace pgg {
 
+#ifndef PGG_SMP_UNIFORM_PDF
+#define PGG_SMP_UNIFORM_PDF 1
+#endif
 #ifndef PGG_SHARE_LANE_HASH
 #define PGG_SHARE_LANE_HASH 1
 #endif
@@ -502,12 +505,26 @@ PGG_HD LaneOut sample_lane(const PixelFrame& pf, bool glossy, float rough, bool 
   o.pdf = 0.0f;
   if (ok) {
     const float bp = co_pos ? brdf_pdf_local(mf, dl, wol) : 0.0f;
+#if PGG_SMP_UNIFORM_PDF
+    // every valid lane maps its direction back to the square, as the
+    // reference does (mixture.py:250-256: hemisphere_to_square of the
+    // direction); one path for Gaussian and BRDF lanes (no divergence)
+    (void)sx;
+    (void)sy;
+    float qx, qy;
+    {
+      V3<float> dz = dl;
+      dz.z = fmaxf(dz.z, 0.0f);
+      dir_to_sq_f(dz, qx, qy);
+    }
+#else
     float qx = sx, qy = sy;
     if (!acc) {
       V3<float> dz = dl;
       dz.z = fmaxf(dz.z, 0.0f);
       dir_to_sq_f(dz, qx, qy);
     }
+#endif
     const float g = gauss_sr(L, qx, qy);
     o.pdf = L.pi * g + (1.0f - L.pi) * bp;
   }
@@ -994,8 +1011,8 @@ PGG_HD void em_partial(const PassArgs& A, const VS& V, const EmSetup& S, int x, 
   constexpr bool kNoBounds = PGG_TILE_OOB && kFull && VS::kZeroOOB;
   for (; s < S.nb; ++s) {
     const uint32_t ua = pcg_out(sa), ub = pcg_out(sb);
-    sa = sa * PCG_MUL + PCG_INC;
-    sb = sb * PCG_MUL + PCG_INC;
+    sa = lcg_step(sa);
+    sb = lcg_step(sb);
     int dx, dy;
     disk_offset_k(ua, ub, C.radius, A.em_radius16, A.em_hband, dx, dy);
     const int cx = x + dx, cy = y + dy;
