@@ -376,9 +376,56 @@ template <class T> PGG_HD V3<T> operator*(const V3<T>& a, T s) { return {a.x * s
 template <class T> PGG_HD V3<T> cross(const V3<T>& a, const V3<T>& b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
+// Fast float64 reciprocal / reciprocal square root for values that are
+// rounded to float32 afterwards: MUFU seed (rcp / rsqrt .approx.f64, ~2^-23)
+// and two Newton steps (~1 ulp of float64) instead of the correctly rounded
+// division / sqrt sequences with their slow-path branches.
+#ifndef PGG_FAST_F64
+#define PGG_FAST_F64 1
+#endif
+PGG_HD double d_rcp(double x) {
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+PGG_HD double d_rsqrt(double x) {
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return fma(y, fma(-h * y, y, 0.5), y);
+#else
+  return 1.0 / sqrt(x);
+#endif
+}
+
+// sqrt / reciprocal for the shared float / double templates: float as
+// before; float64 on the device takes the Newton-refined MUFU seeds (the
+// float64 instances in this TU are the guard-band re-evaluations of float32
+// results, ~1 ulp is ample there)
+PGG_HD float t_sqrt(float x) { return m_sqrt(x); }
+PGG_HD double t_sqrt(double x) {
+#if defined(__CUDA_ARCH__) && PGG_FAST_F64
+  return x > 0.0 ? x * d_rsqrt(x) : 0.0;
+#else
+  return sqrt(x);
+#endif
+}
+PGG_HD float t_rcp(float x) { return 1.0f / x; }
+PGG_HD double t_rcp(double x) { return d_rcp(x); }
+
 template <class T> PGG_HD V3<T> unit(const V3<T>& v) {
-  const T n = m_sqrt(dot(v, v));
-  return v * (T(1) / m_max(n, T(1e-30)));
+  const T n = t_sqrt(dot(v, v));
+  return v * t_rcp(m_max(n, T(1e-30)));
 }
 template <class D, class S> PGG_HD V3<D> cvt(const V3<S>& v) { return {(D)v.x, (D)v.y, (D)v.z}; }
 
@@ -596,29 +643,29 @@ template <class T> PGG_HD V3<T> sample_vndf(T alpha, const V3<T>& wo, uint32_t u
   const T l2 = vh.x * vh.x + vh.y * vh.y;
   V3<T> t1;
   if (l2 > T(1e-18)) {
-    const T inv = T(1) / m_sqrt(l2);
+    const T inv = t_rcp(t_sqrt(l2));
     t1 = {-vh.y * inv, vh.x * inv, T(0)};
   } else {
     t1 = {T(1), T(0), T(0)};
   }
   const V3<T> t2 = cross(vh, t1);
   const T u1 = u01(ua, T());
-  const T r = m_sqrt(u1);
+  const T r = t_sqrt(u1);
   T s, c;
   sincos_turn(ub, &s, &c);
   const T p1 = r * c;
   const T a1 = om_u01(ua, T()) + u1 * s * s;  // 1 - p1^2 without cancellation
   const T sm = T(0.5) * (T(1) + vh.z);
-  const T p2 = (T(1) - sm) * m_sqrt(m_max(a1, T(0))) + sm * (r * s);
+  const T p2 = (T(1) - sm) * t_sqrt(m_max(a1, T(0))) + sm * (r * s);
   const T q = a1 - p2 * p2;
-  const T p3 = m_sqrt(m_max(q, T(0)));
+  const T p3 = t_sqrt(m_max(q, T(0)));
   const V3<T> nh = t1 * p1 + t2 * p2 + vh * p3;
   const V3<T> hv = V3<T>{alpha * nh.x, alpha * nh.y, m_max(nh.z, T(1e-9))};
-  const T hn = m_sqrt(dot(hv, hv));
+  const T hn = t_sqrt(dot(hv, hv));
   // q carries ~1e-7 absolute float32 error; its effect on h is
   // ~1e-7 / (2 p3 |hv|): re-evaluate in float64 where that exceeds ~2e-6
   ill = q < T(1e-3) || p3 * hn < T(0.03);
-  const V3<T> h = hv * (T(1) / m_max(hn, T(1e-30)));
+  const V3<T> h = hv * t_rcp(m_max(hn, T(1e-30)));
   const T k = T(2) * dot(wo, h);
   return h * k - wo;
 }
@@ -641,38 +688,6 @@ struct PixelFrame {
   bool co_pos;      // wo . n > 0 (reference float64 sum order, stored n)
   float om_nn;      // 1 - |n|^2 of the stored normal (kept relative-exact)
 };
-// Fast float64 reciprocal / reciprocal square root for values that are
-// rounded to float32 afterwards: MUFU seed (rcp / rsqrt .approx.f64, ~2^-23)
-// and two Newton steps (~1 ulp of float64) instead of the correctly rounded
-// division / sqrt sequences with their slow-path branches.
-#ifndef PGG_FAST_F64
-#define PGG_FAST_F64 1
-#endif
-PGG_HD double d_rcp(double x) {
-#if defined(__CUDA_ARCH__) && PGG_FAST_F64
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-#else
-  return 1.0 / x;
-#endif
-}
-PGG_HD double d_rsqrt(double x) {
-#if defined(__CUDA_ARCH__) && PGG_FAST_F64
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return fma(y, fma(-h * y, y, 0.5), y);
-#else
-  return 1.0 / sqrt(x);
-#endif
-}
-
 template <class T> PGG_HD Frame<T> make_frame_fast(const V3<T>& n) {
   const T s = m_copysign(T(1), n.z);
   const T a = -d_rcp(s + n.z);

@@ -432,6 +432,9 @@ PGG_HD V3<float> brdf_draw_local(const Mat<float>& mf, float alpha, const V3<flo
                                  uint32_t b, bool& ok) {
   bool ill;
   V3<float> wl = brdf_sample_local<float>(mf, alpha, wol, a, b, ill);
+#ifdef PGG_PROF_NO_VNDF_RECHECK
+  ill = false;  // measurement-only build
+#endif
   if (ill || fabsf(wl.z) < 1e-6f) return brdf_draw_local_d(mf, alpha, wol, co_pos, a, b, ok);
   ok = wl.z > 1e-9f && co_pos;
   return wl;
