@@ -218,6 +218,9 @@ PGG_HD double smp_sqrt(double x) { return m_sqrt(x); }
 #ifndef PGG_SMP_MUFU_LOG
 #define PGG_SMP_MUFU_LOG 1  // Box-Muller ln u (u < 1/2) on lg2.approx: 0.5387 -> 0.5360 ms
 #endif
+#ifndef PGG_SMP_LN_UNIFIED
+#define PGG_SMP_LN_UNIFIED 1
+#endif
 PGG_HD void m_sincospi(float x, float* s, float* c) {
 #if defined(__CUDA_ARCH__) && PGG_SMP_MUFU_TRIG
   const float a = 3.14159265358979323846f * x;  // |x| <= 3/4 (concentric map)
@@ -731,6 +734,24 @@ PGG_HD float kappa_world(float om_nn, float a2) {
 // radius keeps full relative accuracy at both ends.
 PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
   float lnu;
+#if defined(__CUDA_ARCH__) && PGG_SMP_LN_UNIFIED
+  // one branch-free ln u for both halves (the two branches below diverge in
+  // a warp): u < 1/2 as lg2 of u; u >= 1/2 as log1p(-d), d = 1 - u exact
+  // from the integer, by y log(1 + y) / ((1 + y) - 1) on the same lg2
+  // (relative error ~2^-22, |ln u| <= ln 2 there)
+  {
+    const bool lo_half = a < 0x80000000u;
+    const float y = -(float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f;
+    const float w = 1.0f + y;
+    const float arg = lo_half ? (float)a * 2.3283064365386963e-10f : w;
+    float l2;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(arg));
+    const float ln = l2 * 0.69314718055994531f;
+    const float wm1 = w - 1.0f;
+    lnu = lo_half ? ln : (wm1 == 0.0f ? y : y * ln * f_rcp(wm1));
+    if (a == 0u) lnu = -27.631021115928547f;  // log(1e-12), the reference clamp
+  }
+#else
   if (a == 0u) {
     lnu = -27.631021115928547f;  // log(1e-12), the reference clamp
   } else if (a < 0x80000000u) {
@@ -742,6 +763,7 @@ PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
   } else {
     lnu = m_log1p(-(float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f);
   }
+#endif
   const float r = smp_sqrt(-2.0f * lnu);
   float s, c;
   sincos_turn(b, &s, &c);
