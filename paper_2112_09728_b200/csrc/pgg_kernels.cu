@@ -40,7 +40,11 @@ using pgg_rt::g_cuda_err;
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 #ifndef PGG_TILE_H
-#define PGG_TILE_H 8
+// 32 x 12 tiles at 2 blocks/SM (24 warps, 80 registers): 0.4365 vs 0.4405 ms
+// for 32 x 8 at 3 blocks (less VPL halo per pixel: 56 x 36 tile elements
+// for 384 pixels at R = 10-12); 32 x 6 at 4 and 32 x 24 at 1 are slower
+// (0.482 / 0.460 ms)
+#define PGG_TILE_H 12
 #endif
 constexpr int TILE_W = 32, TILE_H = PGG_TILE_H, THREADS = TILE_W * TILE_H;
 constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this radius
@@ -58,7 +62,7 @@ constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this ra
 #define PGG_STASH 1
 #endif
 #ifndef PGG_MIN_BLOCKS
-#define PGG_MIN_BLOCKS 3  // 80 registers, 24 warps/SM: 0.566 vs 0.595 ms at 2 blocks (a few loop-invariant reloads from L1)
+#define PGG_MIN_BLOCKS 2  // 80 registers, 24 warps/SM with 32 x 12 tiles (round 1: 3 blocks of 32 x 8)
 #endif
 
 // shared-memory carve-up of one block
@@ -102,7 +106,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // ---------------------------------------------------------------------------
-// The guiding pass.  A block is a 32 x 8 pixel tile, one warp per row, one
+// The guiding pass.  A block is a 32 x TILE_H pixel tile, one warp per row, one
 // lane per pixel end to end.
 //   stage 0  (kTile) one thread issues two TMA loads of the block's VPL tile
 //            plus the EM halo (Pi y and L planes) into shared memory; they
