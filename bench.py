@@ -851,14 +851,27 @@ def bench_e2e(args, frames, cfg, dev, world):
     from paper_2112_09728_b200.layout import GammaPlanes, GBufferPlanes, SamplePlanes, VplPlanes
     from paper_2112_09728_b200.session import run_pass
 
+    from paper_2112_09728_b200 import _lib, synth
     nh = min(4, SEQ)
     host = []
+    # VPLs cross PCIe in the reference's VplBuffer form (valid, y, radiance,
+    # strategy: 26 B/px, pg/ptrace.py:67-73) and are packed into the kernel's
+    # float4 planes on the device (pgg_pack_vpl); the G-buffer crosses in the
+    # packed planes (65 B/px, no padding)
+    raw = [v for _, v in synth.sequence(W, H, nh, seed=cfg.seed, device=dev)]
     for i in range(nh):
-        g, v = frames[i]
+        g, _ = frames[i]
+        v = raw[i]
         host.append({k: getattr(g, k).cpu().pin_memory() for k in ("flags", "nd", "pr", "va", "am")} |
-                    {"vy": v.y.cpu().pin_memory(), "vl": v.L.cpu().pin_memory(), "cam": g.cam_origin})
+                    {"v_valid": v["valid"].to(torch.uint8).cpu().pin_memory(),
+                     "v_y": v["y"].to(torch.float32).contiguous().cpu().pin_memory(),
+                     "v_rad": v["radiance"].to(torch.float32).contiguous().cpu().pin_memory(),
+                     "v_strat": v["strategy"].to(torch.uint8).cpu().pin_memory(), "cam": g.cam_origin})
+    del raw
     gbs = [GBufferPlanes.empty(H, W, dev) for _ in range(3)]        # cur / prev / next
     vps = [VplPlanes(torch.empty(H, W, 4, device=dev), torch.empty(H, W, 4, device=dev)) for _ in range(2)]
+    vraw = [{k: torch.empty_like(host[0][k], device=dev) for k in ("v_valid", "v_y", "v_rad", "v_strat")}
+            for _ in range(2)]
     gam = [GammaPlanes.fresh(H, W, dev), GammaPlanes.empty(H, W, dev)]
     smps = [SamplePlanes.empty(H, W, args.spp, dev) for _ in range(2)]
     outs = [torch.empty(H, W, 8, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -884,8 +897,8 @@ def bench_e2e(args, frames, cfg, dev, world):
                 s_in.wait_event(cmp_done[(i - 2) % 3])    # slot last read by pass i-1 (as prev) / i-2
             for k in ("flags", "nd", "pr", "va", "am"):
                 getattr(cur, k).copy_(hsrc[k], non_blocking=True)
-            vp.y.copy_(hsrc["vy"], non_blocking=True)
-            vp.L.copy_(hsrc["vl"], non_blocking=True)
+            for k, t in vraw[i % 2].items():
+                t.copy_(hsrc[k], non_blocking=True)
             in_done[i % 3].record(s_in)
         cur.cam_origin = hsrc["cam"]
         o = i % 2
@@ -894,9 +907,12 @@ def bench_e2e(args, frames, cfg, dev, world):
             if i >= 2:
                 s_cmp.wait_event(out_done[o])
             g_in, g_out = gam[st["g"]], gam[1 - st["g"]]
+            r = vraw[i % 2]
+            _lib.check(_lib.lib().pgg_pack_vpl(H * W, _lib.ptr(r["v_valid"]), _lib.ptr(r["v_y"]),
+                                               _lib.ptr(r["v_rad"]), _lib.ptr(r["v_strat"]), _lib.ptr(vp.y),
+                                               _lib.ptr(vp.L), _lib.stream_ptr(s_cmp)))
             run_pass(cfg, i % SEQ, cur, g_in, prev=gbs[(i - 1) % 3] if i > 0 else None, vpl=vp, out_gamma=g_out,
                      out_samples=smps[o], stream=s_cmp)
-            from paper_2112_09728_b200 import _lib
             _lib.check(_lib.lib().pgg_gamma_join(H * W, _lib.ptr(g_out.g0), _lib.ptr(g_out.g1), _lib.ptr(outs[o]),
                                                  _lib.stream_ptr(s_cmp)))
             cmp_done[i % 3].record(s_cmp)
@@ -929,8 +945,9 @@ def bench_e2e(args, frames, cfg, dev, world):
         ms = float(t.item())
     return {"value": world * W * H / (ms * 1e-3) / 1e6, "unit": "Mpixels/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
-            "path": "pinned host packed planes -> H2D -> pgg_guiding_pass -> pgg_gamma_join + samples -> D2H, "
-                    "3 streams (copy-in / pass / copy-out) overlapping adjacent frames"}
+            "path": "pinned host: G-buffer planes + the reference's VplBuffer fields -> H2D -> pgg_pack_vpl -> "
+                    "pgg_guiding_pass -> pgg_gamma_join + samples -> D2H, 3 streams (copy-in / pass / copy-out) "
+                    "overlapping adjacent frames"}
 
 
 def main():
