@@ -232,8 +232,9 @@ def workload_stats(frames, gamma):
     dev = st.device
     e = lambda *s: torch.empty(*s, dtype=torch.float64, device=dev)  # noqa: E731
     reset = torch.empty(n, dtype=torch.uint8, device=dev)
-    _lib.check(_lib.lib().pgg_lobe(n, _lib.ptr(st), _lib.ptr(e(n, 2)), _lib.ptr(e(n, 4)), _lib.ptr(e(n, 4)),
-                                   _lib.ptr(e(n)), _lib.ptr(reset), _lib.stream_ptr()))
+    outs = [e(n, 2), e(n, 4), e(n, 4), e(n)]  # kept alive: a temporary's block could be reused by the next
+    _lib.check(_lib.lib().pgg_lobe(n, _lib.ptr(st), *[_lib.ptr(o) for o in outs], _lib.ptr(reset),
+                                   _lib.stream_ptr()))
     v_last = valid[(len(frames) - 1)].reshape(-1)
     return {"invalid_fraction": round(1.0 - valid.float().mean().item(), 4),
             "history_fraction": round(hist.float().mean().item() / max(valid.float().mean().item(), 1e-9), 4),

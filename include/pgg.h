@@ -357,6 +357,13 @@ int pgg_debug_checks(int32_t* host_out6, int32_t reset);
 int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream);
 int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
                         int32_t* rechecks, void* stream);
+/*   pgg_debug_brdf_draw   the sampler's local-frame BRDF draw (Lambert cosine
+ *       or GGX VNDF, scene.py:311-351, with the float64 re-evaluation of rim
+ *       samples) for n lanes: glossy u8, roughness, wo float4 (local), draws
+ *       (u1, u2) as u32 pairs; out float4 (wi.xyz, valid); *rechecks += the
+ *       draws re-evaluated in float64 */
+int pgg_debug_brdf_draw(int64_t n, const uint8_t* glossy, const float* rough, const float* wo, const uint32_t* draws,
+                        float* out, int32_t* rechecks, void* stream);
 int pgg_debug_reproject(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
                         const pgg_gamma_in* gamma_prev, uint8_t* decisions, void* stream);
 

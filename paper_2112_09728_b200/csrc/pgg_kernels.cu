@@ -662,6 +662,28 @@ __global__ void k_debug_bm_accept(int64_t n, int per, const float* __restrict__ 
   count_add(rechecks, c);
 }
 
+// local-frame BRDF draws of the sampler (brdf_draw_local: Lambert cosine or
+// GGX VNDF with the float64 rim re-evaluation), one per lane: glossy[i],
+// roughness[i], wo (float4 local, w unused), raw draws (a, b)
+__global__ void k_debug_brdf_draw(int64_t n, const uint8_t* __restrict__ glossy, const float* __restrict__ rough,
+                                  const float4* __restrict__ wo, const uint32_t* __restrict__ ab,
+                                  float4* __restrict__ out, int32_t* rechecks) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int c = 0;
+  if (i < n) {
+    const double r2d = (double)rough[i] * (double)rough[i];
+    const float alpha = (float)fmax(r2d, 1e-6);
+    const float a2 = alpha * alpha;
+    const Mat<float> mf{glossy[i] != 0, a2, a2};
+    const float4 w = wo[i];
+    const V3<float> wol = v3(w.x, w.y, w.z);
+    bool ok;
+    const V3<float> d = brdf_draw_local(mf, alpha, wol, w.z > 0.0f, ab[2 * i], ab[2 * i + 1], ok, &c);
+    out[i] = f4(d.x, d.y, d.z, ok ? 1.0f : 0.0f);
+  }
+  count_add(rechecks, c);
+}
+
 // reprojection decision record of every pixel of the call's band
 __global__ void k_debug_reproject(const PassArgs A, uint8_t* __restrict__ out) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -939,6 +961,16 @@ int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const u
   if (n == 0) return PGG_OK;
   if (const int rc = device_check()) return rc;
   k_debug_bm_accept<<<blocks(n, 256), 256, 0, S(stream)>>>(n, per_lobe, stats, draws, out, rechecks);
+  return check_launch();
+}
+
+int pgg_debug_brdf_draw(int64_t n, const uint8_t* glossy, const float* rough, const float* wo, const uint32_t* draws,
+                        float* out, int32_t* rechecks, void* stream) {
+  if (n < 0 || !glossy || !rough || !wo || !draws || !out || !rechecks) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_debug_brdf_draw<<<blocks(n, 256), 256, 0, S(stream)>>>(n, glossy, rough, reinterpret_cast<const float4*>(wo),
+                                                           draws, reinterpret_cast<float4*>(out), rechecks);
   return check_launch();
 }
 

@@ -429,13 +429,16 @@ PGG_COLD V3<float> brdf_draw_local_d(const Mat<float>& mf, float alpha, const V3
 // local-frame BRDF draw with its validity (wl.z > 1e-9, wo.z > 0); float64
 // re-evaluation for the VNDF rim case and near the z threshold
 PGG_HD V3<float> brdf_draw_local(const Mat<float>& mf, float alpha, const V3<float>& wol, bool co_pos, uint32_t a,
-                                 uint32_t b, bool& ok) {
+                                 uint32_t b, bool& ok, int* rechecks = nullptr) {
   bool ill;
   V3<float> wl = brdf_sample_local<float>(mf, alpha, wol, a, b, ill);
 #ifdef PGG_PROF_NO_VNDF_RECHECK
   ill = false;  // measurement-only build
 #endif
-  if (ill || fabsf(wl.z) < 1e-6f) return brdf_draw_local_d(mf, alpha, wol, co_pos, a, b, ok);
+  if (ill || fabsf(wl.z) < 1e-6f) {
+    if (rechecks) ++*rechecks;
+    return brdf_draw_local_d(mf, alpha, wol, co_pos, a, b, ok);
+  }
   ok = wl.z > 1e-9f && co_pos;
   return wl;
 }
