@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-frame-loop", action="store_true")
     ap.add_argument("--bands", action="store_true", help="row-band path even at N=1 (exercises the NCCL code)")
     ap.add_argument("--no-bands", action="store_true", help="N>1: skip the 4K 4 spp row-band leg")
+    ap.add_argument("--with-bands-leg", action="store_true",
+                    help="run the N>1 row-band leg also at N=1 (under torchrun; exercises that code path)")
     ap.add_argument("--seq", type=int, default=0,
                     help="time one true N-frame sequence (frames generated on the device between passes, "
                          "not timed) instead of cycling 16 resident frames; BASELINE configs[4] is --workload 8k "
@@ -642,7 +644,7 @@ def bench_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         e2e = bench_e2e(args, frames, cfg, dev, world)
     bands = None
-    if world > 1 and not args.no_bands:
+    if (world > 1 or args.with_bands_leg) and not args.no_bands:
         # the strong-scaling leg of the same run: one 4K 4 spp frame over N
         # row bands with the NCCL halo exchange (BASELINE configs[3])
         frames.clear()
@@ -979,7 +981,7 @@ def main():
     if torch.cuda.device_count() <= local_rank:
         sys.exit(f"bench.py: rank {rank}: LOCAL_RANK={local_rank} but only {torch.cuda.device_count()} "
                  "CUDA device(s) are visible")
-    use_dist = world > 1 or args.bands
+    use_dist = world > 1 or args.bands or args.with_bands_leg
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
