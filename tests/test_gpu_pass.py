@@ -203,21 +203,23 @@ def _ns(d):
 BANDS_1080P = ((0, 48), (516, 564), (1032, 1080))  # top edge, middle, bottom edge
 
 
-def test_1080p_vs_oracle(cuda_dev):
+@pytest.mark.parametrize("F", [5, 13])
+def test_1080p_vs_oracle(cuda_dev, F):
     """The benchmarked configuration (BASELINE configs[1]/[2]: 1920x1080,
     1 spp, reproject + depth-0 sampling/pdf (MIS) + EM, disocclusions from
     the panning camera and the hole pattern) against the CPU oracle on three
     full-width row bands -- the top and bottom frame edges and the middle --
     with the whole frame as context (pg/guide_buffers.py:262-283, 78-137;
-    pg/ptrace.py:161-220).  Gamma comes from four GPU frames of the bench
+    pg/ptrace.py:161-220).  Gamma comes from F - 1 GPU frames of the bench
     sequence (trained lobes: correlated, reset, k up to 4) and is fed to both
-    sides.  Single-kernel policy: Gamma p99.99 <= 1e-4, max <=
+    sides (F - 1 = 4 and 12 frames: k up to 4 / 12, EM budgets 20 down to
+    17).  Single-kernel policy: Gamma p99.99 <= 1e-4, max <=
     1e-3, k exact; samples: tags and validity exact, directions <= 1e-5,
     pdf p99.99 <= 1e-4."""
     from paper_2112_09728_b200 import synth
     from paper_2112_09728_b200.session import GuidingSession
     GammaPlanes, GBufferPlanes, PassConfig, VplPlanes, run_pass = _api()
-    w, h, seed, F = 1920, 1080, 0, 5
+    w, h, seed = 1920, 1080, 0
     frames = list(synth.sequence(w, h, F, seed=seed, device=cuda_dev))
     cfg = PassConfig(seed=seed, spp=1)
     sess = GuidingSession(w, h, cfg, device=cuda_dev)
