@@ -279,7 +279,8 @@ int pgg_render_pass(const pgg_render_config* cfg, const pgg_scene* scene, const 
  *                         2 brdf_sample -> wi, pdf, valid (two draws)
  *                         (scene.py:258-380)
  *   pgg_primary_rays .... scene.primary_ray_dirs (scene.py:125-135)
- *   pgg_project ......... scene.project_to_pixels (scene.py:138-151) */
+ *   pgg_project ......... scene.project_to_pixels (scene.py:138-151)
+ *   pgg_motion_vectors .. ptrace.motion_vectors (ptrace.py:132-150) */
 int pgg_intersect(const pgg_scene* scene, int64_t n, const double* origins, const double* dirs, const double* t_min,
                   const double* t_max, int32_t any_hit, uint8_t* hit, double* t, double* pos, double* normal,
                   int32_t* mat, uint8_t* front, void* stream);
@@ -292,6 +293,11 @@ int pgg_primary_rays(const pgg_camera* cam, int32_t width, int32_t height, int64
                      const double* py, double* dirs, void* stream);
 int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n, const double* points, double* px,
                 double* py, uint8_t* in_front, void* stream);
+/* ptrace.motion_vectors (ptrace.py:132-150) for a caller G-buffer: pos is
+ * height x width x 3 hit points, valid its hit mask; writes motion (height x
+ * width x 2, zero where no history) and has_history. */
+int pgg_motion_vectors(const pgg_camera* prev_cam, int32_t width, int32_t height, const double* pos,
+                       const uint8_t* valid, double* motion, uint8_t* has_history, void* stream);
 
 /* sgmap.py:21-115 as float64 lane operations: op 0 square_to_disk (n x 2 ->
  * n x 2), 1 disk_to_square (2 -> 2), 2 square_to_hemisphere (2 -> 3),

@@ -111,6 +111,7 @@ _SIGS = {
     "pgg_primary_rays": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p],
     "pgg_sgmap": [c_i32, c_i64, c_p, c_p, c_p],
     "pgg_project": [ctypes.POINTER(Camera), c_i32, c_i32, c_i64, c_p, c_p, c_p, c_p, c_p],
+    "pgg_motion_vectors": [ctypes.POINTER(Camera), c_i32, c_i32, c_p, c_p, c_p, c_p, c_p],
     "pgg_mixture_lanes": [c_i32, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i32, c_p],
     "pgg_sample_gauss": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_debug_checks": [c_p, c_i32],

@@ -352,6 +352,21 @@ struct GbArgs {
 
 __device__ __forceinline__ D3 cam3(const double* v) { return d3(v[0], v[1], v[2]); }
 
+// scene.project_to_pixels (pg/scene.py:138-151) of one point: continuous pixel
+// coordinates in camera `c`'s frame; returns in_front (z > 1e-9)
+__device__ __forceinline__ bool project_px(const pgg_camera& c, int w, int h, const D3 p, double& px, double& py) {
+  const double aspect = (double)w / (double)h;
+  const D3 dd = p - cam3(c.origin);
+  const double zc = dot(dd, cam3(c.forward));
+  const bool fr = zc > 1e-9;
+  const double z = fr ? zc : 1.0;
+  const double xc = dot(dd, cam3(c.right)) / z;
+  const double yc = dot(dd, cam3(c.up)) / z;
+  px = (xc / (c.tan_half_fov * aspect) + 1.0) * 0.5 * (double)w - 0.5;
+  py = (1.0 - yc / c.tan_half_fov) * 0.5 * (double)h - 0.5;
+  return fr;
+}
+
 __global__ void __launch_bounds__(128) k_gbuffer(const GbArgs A) {
   extern __shared__ double smem[];
   const SceneS S = stage_scene(A.scene, smem);
@@ -382,15 +397,8 @@ __global__ void __launch_bounds__(128) k_gbuffer(const GbArgs A) {
   bool has = false;
   if (A.has_prev) {
     // previous camera's projection of the hit (pg/scene.py:138-151, pg/ptrace.py:132-150)
-    const D3 dd = h.pos - cam3(A.prev.origin);
-    const double zc = dot(dd, cam3(A.prev.forward));
-    const bool in_front = zc > 1e-9;
-    const double z = in_front ? zc : 1.0;
-    const double xc = dot(dd, cam3(A.prev.right)) / z;
-    const double yc = dot(dd, cam3(A.prev.up)) / z;
-    const double pth = A.prev.tan_half_fov;
-    const double px = (xc / (pth * aspect) + 1.0) * 0.5 * (double)A.W - 0.5;
-    const double py = (1.0 - yc / pth) * 0.5 * (double)A.H - 0.5;
+    double px, py;
+    const bool in_front = project_px(A.prev, A.W, A.H, h.pos, px, py);
     const double tx = rint(px), ty = rint(py);
     has = in_front && tx >= 0.0 && tx < (double)A.W && ty >= 0.0 && ty < (double)A.H;
     if (has) {
@@ -779,16 +787,27 @@ __global__ void k_lane_project(pgg_camera cam, int w, int h, int64_t n, const do
                                uint8_t* in_front) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double aspect = (double)w / (double)h;
-  const D3 dd = ldd3(pts, i) - cam3(cam.origin);
-  const double zc = dot(dd, cam3(cam.forward));
-  const bool fr = zc > 1e-9;
-  const double z = fr ? zc : 1.0;
-  const double xc = dot(dd, cam3(cam.right)) / z;
-  const double yc = dot(dd, cam3(cam.up)) / z;
-  px[i] = (xc / (cam.tan_half_fov * aspect) + 1.0) * 0.5 * (double)w - 0.5;
-  py[i] = (1.0 - yc / cam.tan_half_fov) * 0.5 * (double)h - 0.5;
+  double x, y;
+  const bool fr = project_px(cam, w, h, ldd3(pts, i), x, y);
+  px[i] = x;
+  py[i] = y;
   in_front[i] = fr ? 1 : 0;
+}
+
+// ptrace.motion_vectors (pg/ptrace.py:132-150) over a caller G-buffer's hit
+// points: offset to the previous camera's projection where the pixel is
+// valid, in front of that camera and rounds (np.rint) inside the frame
+__global__ void k_motion_vectors(pgg_camera prev, int w, int h, const double* pos, const uint8_t* valid,
+                                 double* motion, uint8_t* has) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)w * h) return;
+  double px, py;
+  const bool fr = project_px(prev, w, h, ldd3(pos, i), px, py);
+  const double tx = rint(px), ty = rint(py);
+  const bool ok = valid[i] && fr && tx >= 0.0 && tx < (double)w && ty >= 0.0 && ty < (double)h;
+  motion[2 * i] = ok ? px - (double)(i % w) : 0.0;
+  motion[2 * i + 1] = ok ? py - (double)(i / w) : 0.0;
+  has[i] = ok ? 1 : 0;
 }
 
 
@@ -999,6 +1018,17 @@ int pgg_project(const pgg_camera* cam, int32_t width, int32_t height, int64_t n,
   if (const int rc = pgg_rt::device_check()) return rc;
   k_lane_project<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*cam, width, height, n, points,
                                                                                      px, py, in_front);
+  return pgg_rt::check_launch();
+}
+
+int pgg_motion_vectors(const pgg_camera* prev_cam, int32_t width, int32_t height, const double* pos,
+                       const uint8_t* valid, double* motion, uint8_t* has_history, void* stream) {
+  if (!prev_cam || width < 0 || height < 0 || !pos || !valid || !motion || !has_history) return PGG_ERR_ARGUMENT;
+  const int64_t n = (int64_t)width * height;
+  if (n == 0) return PGG_OK;
+  if (const int rc = pgg_rt::device_check()) return rc;
+  k_motion_vectors<<<lane_blocks(n), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*prev_cam, width, height, pos,
+                                                                                       valid, motion, has_history);
   return pgg_rt::check_launch();
 }
 

@@ -194,28 +194,21 @@ def gbuffer_pass(scene, frame_index, resolution):
 
 def motion_vectors(prev_cam, cur_cam, gbuf):
     """Offsets to the previous camera's projection of every valid hit
-    (pg/ptrace.py:132-150; pg/scene.py:138-151), float64 on the device."""
-    dev = _conv.device()
+    (pg/ptrace.py:132-150; pg/scene.py:138-151): one float64 lane kernel
+    (pgg_motion_vectors) over the caller's G-buffer."""
+    import ctypes
+
+    from . import _lib
+    from .render import camera_abi
     h, w = gbuf.height, gbuf.width
-    f64 = torch.float64
-    pos = _conv.to_dev(gbuf.pos, f64).reshape(-1, 3)
-    t = lambda v: torch.as_tensor(np.asarray(v, dtype=np.float64), device=dev)  # noqa: E731
-    d = pos - t(prev_cam.origin)
-    zc = d @ t(prev_cam.forward)
-    front = zc > 1e-9
-    z = torch.where(front, zc, torch.ones_like(zc))
-    xc = (d @ t(prev_cam.right)) / z
-    yc = (d @ t(prev_cam.up)) / z
-    aspect = w / float(h)
-    px = ((xc / (prev_cam.tan_half_fov * aspect) + 1.0) * 0.5 * w - 0.5).reshape(h, w)
-    py = ((1.0 - yc / prev_cam.tan_half_fov) * 0.5 * h - 0.5).reshape(h, w)
-    ii, jj = torch.meshgrid(torch.arange(h, device=dev, dtype=f64), torch.arange(w, device=dev, dtype=f64),
-                            indexing="ij")
-    tx, ty = torch.round(px), torch.round(py)  # half-to-even like np.rint
-    valid = _conv.to_dev(gbuf.valid, torch.bool)
-    has = valid & front.reshape(h, w) & (tx >= 0) & (tx < w) & (ty >= 0) & (ty < h)
-    zero = torch.zeros_like(px)
-    m = torch.stack([torch.where(has, px - jj, zero), torch.where(has, py - ii, zero)], dim=-1)
+    pos = _conv.to_dev(gbuf.pos, torch.float64).reshape(h, w, 3).contiguous()
+    valid = _conv.to_dev(gbuf.valid, torch.bool).reshape(h, w).to(torch.uint8).contiguous()
+    m = torch.empty(h, w, 2, dtype=torch.float64, device=pos.device)
+    has = torch.empty(h, w, dtype=torch.uint8, device=pos.device)
+    c = camera_abi(prev_cam)
+    _lib.check(_lib.lib().pgg_motion_vectors(ctypes.byref(c), int(w), int(h), _lib.ptr(pos), _lib.ptr(valid),
+                                             _lib.ptr(m), _lib.ptr(has), _lib.stream_ptr()))
+    has = has.bool()
     if _conv.is_torch(gbuf.pos):
         return m, has
     return m.cpu().numpy(), has.cpu().numpy()

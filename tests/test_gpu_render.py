@@ -72,6 +72,32 @@ def test_gbuffer_matches_reference(cuda_dev, case):
     np.testing.assert_allclose(gb.view[~v], z["gb_view"][~v], rtol=1e-6, atol=1e-7)
 
 
+@pytest.mark.parametrize("case", CASES)
+def test_motion_vectors_on_reference_gbuffer(cuda_dev, case):
+    """ptrace.motion_vectors (pgg_motion_vectors kernel) on the reference's
+    own float64 hit points vs its motion/has_history (pg/ptrace.py:132-150):
+    has_history exact, offsets within 1e-9 px (float64 operation order)."""
+    from paper_2112_09728_b200 import ptrace
+    from paper_2112_09728_b200 import scene as S
+    z = gio.load(f"render_{case}.npz")
+    sc = _scene(z)
+    fr = int(z["frame"])
+    if fr == 0:
+        pytest.skip("frame 0 has no previous camera")
+    h, w = z["gb_valid"].shape
+    gb = SimpleNamespace(width=w, height=h, pos=z["gb_pos"], valid=z["gb_valid"])
+    m, has = ptrace.motion_vectors(S.camera_at(sc, fr - 1), S.camera_at(sc, fr), gb)
+    np.testing.assert_array_equal(has, z["gb_has_history"])
+    assert has.any()
+    np.testing.assert_allclose(m, z["gb_motion"], rtol=0, atol=1e-9)
+    # torch in -> torch out on the device
+    mt, ht = ptrace.motion_vectors(S.camera_at(sc, fr - 1), S.camera_at(sc, fr),
+                                   SimpleNamespace(width=w, height=h, pos=torch.as_tensor(z["gb_pos"], device=cuda_dev),
+                                                   valid=torch.as_tensor(z["gb_valid"], device=cuda_dev)))
+    assert mt.is_cuda and ht.dtype == torch.bool
+    np.testing.assert_array_equal(mt.cpu().numpy(), m)
+
+
 def _render_case(z, mode, cuda_dev):
     from paper_2112_09728_b200 import ptrace
     sc = _scene(z)
