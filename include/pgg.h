@@ -349,7 +349,7 @@ int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double
  *   pgg_debug_bm_accept   Box-Muller proposal acceptance p in [0,1]^2
  *       (mixture.py:216-230) for n proposals, lobe i / per_lobe from float32
  *       Gamma stats[8]; draws (u1, u2) as u32 pairs; out bit0 accepted, bit1
- *       re-decided in float64
+ *       re-decided in float64; proposals (nullable) the float32 p = mu + L z
  *   pgg_debug_reproject   reprojection decision per pixel of cfg's band
  *       (guide_buffers.py:78-137): bit0 accepted, bit1 gates re-decided in
  *       float64, bit2 rejected by the mean rotation (z < 0), bit3 rejected by
@@ -362,7 +362,7 @@ int pgg_sample_gauss(int64_t n, const double* pi, const double* mu, const double
 int pgg_debug_checks(int32_t* host_out6, int32_t reset);
 int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream);
 int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
-                        int32_t* rechecks, void* stream);
+                        float* proposals, int32_t* rechecks, void* stream);
 /*   pgg_debug_brdf_draw   the sampler's local-frame BRDF draw (Lambert cosine
  *       or GGX VNDF, scene.py:311-351, with the float64 re-evaluation of rim
  *       samples) for n lanes: glossy u8, roughness, wo float4 (local), draws

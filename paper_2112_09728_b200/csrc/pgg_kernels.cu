@@ -640,7 +640,7 @@ __global__ void k_debug_em_offsets(const PassArgs A, int8_t* __restrict__ out, i
 // Box-Muller proposals of the guided branch: lobe from float32 Gamma
 // (make_lobe, as pixel_stage), acceptance via bm_propose
 __global__ void k_debug_bm_accept(int64_t n, int per, const float* __restrict__ stats, const uint32_t* __restrict__ ab,
-                                  uint8_t* __restrict__ out, int32_t* rechecks) {
+                                  uint8_t* __restrict__ out, float* __restrict__ p_out, int32_t* rechecks) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int c = 0;
   if (i < n) {
@@ -657,6 +657,10 @@ __global__ void k_debug_bm_accept(int64_t n, int per, const float* __restrict__ 
     float px, py;
     const bool in = bm_propose(L, cd, ab[2 * i], ab[2 * i + 1], px, py, &rc);
     out[i] = (uint8_t)((in ? 1 : 0) | (rc ? 2 : 0));
+    if (p_out) {
+      p_out[2 * i] = px;
+      p_out[2 * i + 1] = py;
+    }
     c = rc ? 1 : 0;
   }
   count_add(rechecks, c);
@@ -956,11 +960,11 @@ int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechec
 }
 
 int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
-                        int32_t* rechecks, void* stream) {
+                        float* proposals, int32_t* rechecks, void* stream) {
   if (n < 0 || per_lobe < 1 || !stats || !draws || !out || !rechecks) return PGG_ERR_ARGUMENT;
   if (n == 0) return PGG_OK;
   if (const int rc = device_check()) return rc;
-  k_debug_bm_accept<<<blocks(n, 256), 256, 0, S(stream)>>>(n, per_lobe, stats, draws, out, rechecks);
+  k_debug_bm_accept<<<blocks(n, 256), 256, 0, S(stream)>>>(n, per_lobe, stats, draws, out, proposals, rechecks);
   return check_launch();
 }
 

@@ -777,20 +777,23 @@ PGG_HD float kappa_world(float om_nn, float a2) {
 PGG_HD void box_muller_f(uint32_t a, uint32_t b, float& z0, float& z1) {
   float lnu;
 #if defined(__CUDA_ARCH__) && PGG_SMP_LN_UNIFIED
-  // one branch-free ln u for both halves (the two branches below diverge in
-  // a warp): u < 1/2 as lg2 of u; u >= 1/2 as log1p(-d), d = 1 - u exact
-  // from the integer, by y log(1 + y) / ((1 + y) - 1) on the same lg2
-  // (relative error ~2^-22, |ln u| <= ln 2 there)
+  // one branch-free ln u for the whole range (branches diverge in a warp).
+  // u < 3/4: lg2.approx of u -- its error is ABSOLUTE (~2^-22), so only
+  // where |ln u| >= 0.287 is it a small relative error (<= 4e-7).
+  // u >= 3/4: log1p(-d) with d = 1 - u exact from the integer, as
+  // 2 atanh(s), s = -d / (2 - d), |s| <= 1/7: four odd terms (truncation
+  // < 2e-8 relative).  Near u = 1 (r = sqrt(-2 ln u) -> 0) this keeps r
+  // relatively accurate; a log of 1 - d on lg2 would not (0.999999688:
+  // 40 % error in ln u, 3.5e-5 in the sampled direction).
   {
-    const bool lo_half = a < 0x80000000u;
-    const float y = -(float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f;
-    const float w = 1.0f + y;
-    const float arg = lo_half ? (float)a * 2.3283064365386963e-10f : w;
+    const bool lo = a < 0xC0000000u;
     float l2;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(arg));
-    const float ln = l2 * 0.69314718055994531f;
-    const float wm1 = w - 1.0f;
-    lnu = lo_half ? ln : (wm1 == 0.0f ? y : y * ln * f_rcp(wm1));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"((float)a * 2.3283064365386963e-10f));
+    const float d = (float)(0x100000000ULL - (uint64_t)a) * 2.3283064365386963e-10f;
+    const float sd = -d * f_rcp(2.0f - d);
+    const float t = sd * sd;
+    const float p = fmaf(t, fmaf(t, fmaf(t, 0.14285714285714285f, 0.2f), 0.33333333333333333f), 1.0f);
+    lnu = lo ? l2 * 0.69314718055994531f : 2.0f * sd * p;
     if (a == 0u) lnu = -27.631021115928547f;  // log(1e-12), the reference clamp
   }
 #else

@@ -100,22 +100,38 @@ def _random_stats(n, rng):
 
 
 def test_box_muller_acceptance_10m(cuda_dev):
-    """10.5 M Box-Muller proposals (2.1 M lobes x 5 draw pairs): the device's
+    """10.5 M Box-Muller proposals (2.1 M lobes x 5 draw pairs, 5 % with u1
+    within 2^-12 of 1, 1 % around the device ln's 3/4 switch): the device's
     float32 acceptance with float64 edge recheck equals the reference's
-    float64 decision on every proposal."""
+    float64 decision on every proposal, and the proposal p = mu + L z is
+    within 1e-6 (1 + |L z|) of the float64 one (1e-6 absolute where
+    u1 -> 1 and the radius -> 0)."""
     from paper_2112_09728_b200 import _lib
     rng = np.random.default_rng(11)
     nl, per = 2_100_000, 5
     st = _random_stats(nl, rng)
-    ab = rng.integers(0, 2**32, (nl * per, 2), dtype=np.uint64).astype(np.uint32)
+    ab = rng.integers(0, 2**32, (nl * per, 2), dtype=np.uint64)
+    # u1 near 1 (radius -> 0: ln u needs relative accuracy there) and around
+    # the 3/4 switch of the device's ln; u1 = 0 (the reference's 1e-12 clamp)
+    k = rng.random(nl * per)
+    ab[:, 0] = np.where(k < 0.05, 2**32 - rng.integers(1, 2**20, nl * per, dtype=np.uint64), ab[:, 0])
+    ab[:, 0] = np.where((k >= 0.05) & (k < 0.06),
+                        np.uint64(0xC0000000) + rng.integers(-4096, 4096, nl * per).astype(np.int64).astype(np.uint64),
+                        ab[:, 0])
+    ab[:16, 0] = 0
+    ab = ab.astype(np.uint32)
     out = torch.empty(nl * per, dtype=torch.uint8, device=cuda_dev)
+    prop = torch.empty(nl * per, 2, dtype=torch.float32, device=cuda_dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
     st_d = torch.from_numpy(st).to(cuda_dev)
     ab_d = torch.from_numpy(ab.view(np.int32)).to(cuda_dev)
     _lib.check(_lib.lib().pgg_debug_bm_accept(nl * per, per, _lib.ptr(st_d), _lib.ptr(ab_d), _lib.ptr(out),
-                                              _lib.ptr(cnt), _lib.stream_ptr()))
+                                              _lib.ptr(prop), _lib.ptr(cnt), _lib.stream_ptr()))
     got = out.cpu().numpy()
+    gp = prop.cpu().numpy().astype(np.float64)
     bad = 0
+    worst = 0.0       # max |p - p64| / (1e-6 (1 + |L z|_1)) over all proposals
+    worst_near1 = 0.0  # max |p - p64| where u1 > 1 - 2^-12 (|L z| <= 0.02)
     chunk = 1 << 18
     for a in range(0, nl, chunk):
         b = min(nl, a + chunk)
@@ -137,10 +153,18 @@ def test_box_muller_acceptance_10m(cuda_dev):
         py = rep(my) + rep(l21) * g0 + rep(l22) * g1
         inside = (px >= 0.0) & (px <= 1.0) & (py >= 0.0) & (py <= 1.0)
         bad += int(np.count_nonzero(inside != (got[a * per:b * per] & 1).astype(bool)))
+        e = np.maximum(np.abs(gp[a * per:b * per, 0] - px), np.abs(gp[a * per:b * per, 1] - py))
+        lz = np.abs(rep(l11) * g0) + np.abs(rep(l21) * g0) + np.abs(rep(l22) * g1)
+        worst = max(worst, float(np.max(e / (1e-6 * (1.0 + lz)))))
+        n1 = u[:, 0] > 1.0 - 2.0 ** -12
+        if n1.any():
+            worst_near1 = max(worst_near1, float(e[n1].max()))
     rec = {"proposals": nl * per, "mismatches": bad, "f64_rechecks": int(cnt.item()),
-           "accepted": int(np.count_nonzero(got & 1))}
+           "accepted": int(np.count_nonzero(got & 1)), "p_err_rel_1e6_max": worst,
+           "p_abs_err_max_u1_near_1": worst_near1}
     _report("box_muller_accept", rec)
     assert bad == 0, rec
+    assert worst <= 1.0 and worst_near1 <= 1e-6, rec
     assert cnt.item() > 0
 
 

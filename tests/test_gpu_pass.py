@@ -248,3 +248,44 @@ def test_1080p_vs_oracle(cuda_dev, F):
         band = slice(r0 * w, r1 * w)
         check_samples({k: v[band] for k, v in smp.items()}, osmp["wi"], osmp["pdf"], osmp["strategy"],
                       osmp["valid"])
+
+
+
+BANDS_4K = ((0, 16), (1072, 1088), (2144, 2160))
+
+
+def test_4k_4spp_vs_oracle(cuda_dev):
+    """BASELINE configs[3]'s pass (3840x2160, 4 spp: four depth-0 lanes per
+    pixel, each with its own PCG stream, and their MIS pdfs) against the CPU
+    oracle on three full-width 16-row bands (top edge, middle, bottom edge)
+    with the whole frame as context, after 4 GPU frames of the 4K sequence.
+    Same single-kernel policy as test_1080p_vs_oracle."""
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.session import GuidingSession
+    GammaPlanes, GBufferPlanes, PassConfig, VplPlanes, run_pass = _api()
+    w, h, seed, spp, F = 3840, 2160, 0, 4, 5
+    frames = list(synth.sequence(w, h, F, seed=seed, device=cuda_dev))
+    cfg = PassConfig(seed=seed, spp=spp)
+    sess = GuidingSession(w, h, cfg, device=cuda_dev)
+    for f in range(F - 1):
+        g, v = frames[f]
+        sess.step(GBufferPlanes.from_ref(g, device=cuda_dev), VplPlanes.from_ref(v, device=cuda_dev), f)
+    gin = sess.gamma.to_aos().cpu().numpy()
+    (gp, _), (gc, vc) = frames[F - 2], frames[F - 1]
+    miss = torch.zeros(1, dtype=torch.int32, device=cuda_dev)
+    r = run_pass(cfg, F - 1, GBufferPlanes.from_ref(gc, device=cuda_dev), GammaPlanes.from_aos(gin, cuda_dev),
+                 prev=GBufferPlanes.from_ref(gp, device=cuda_dev), vpl=VplPlanes.from_ref(vc, device=cuda_dev),
+                 halo_misses=miss)
+    got = r.gamma.to_aos().cpu().numpy()
+    smp = _samples(r, w * h, spp)
+    assert int(miss.item()) == 0
+    gpn, gcn, vcn = _ns(gp), _ns(gc), _ns(vc)
+    assert (gin[..., 7] >= 1).mean() > 0.5
+    for r0, r1 in BANDS_4K:
+        _, osmp, otr = O.guiding_frame(gin, gpn, gcn, vcn, seed, F - 1, spp=spp, rows=(r0, r1))
+        check_gamma(got[r0:r1], otr)
+        band = slice(r0 * w, r1 * w)
+        sb = {k: v[band] for k, v in smp.items()}
+        assert osmp["wi"].shape == sb["wi"].shape
+        check_samples(sb, osmp["wi"], osmp["pdf"], osmp["strategy"], osmp["valid"])
+        assert sb["strategy"].any() and not sb["strategy"].all()
