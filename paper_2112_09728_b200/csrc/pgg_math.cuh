@@ -727,6 +727,9 @@ template <class T> PGG_HD V3<T> brdf_sample_local(const Mat<T>& m, T alpha, cons
 // Tangent frame and local view of a pixel: built in float64 and rounded, so
 // small local components (view near the normal, directions near the
 // horizon) keep their relative precision in the float32 math downstream.
+#ifndef PGG_WOL_RAW_FRAME
+#define PGG_WOL_RAW_FRAME 2  // 1: always the raw-frame view (+0.2 %), 2: only within 0.1 of n (+0.07 %)
+#endif
 struct PixelFrame {
   Frame<float> fr;  // orthonormal frame about n/|n|
   V3<float> wol;    // view in that frame
@@ -759,7 +762,33 @@ PGG_HD PixelFrame make_pixel_frame(const V3<float>& n, const V3<float>& wo) {
   p.fr.t = cvt<float>(fd.t);
   p.fr.b = cvt<float>(fd.b);
   p.fr.n = cvt<float>(nh);
+#if PGG_WOL_RAW_FRAME
+  // the local view as the reference forms it: in the frame of the STORED
+  // normal (sgmap.build_tangent_frame / to_local of the raw n, ptrace.py:
+  // 200-202, scene.py:354-380).  A float32 normal has |n| = 1 +- 1e-7, and
+  // that frame's t, b are then off-orthogonal to n by ~|n|^2 - 1: when the
+  // view is within ~1e-3 of n the azimuth of (wo.x, wo.y) -- which the VNDF
+  // sample rotates with -- moves by ~1e-4 between the raw and the
+  // normalised frame (4K sequence: 7e-5 direction error).  Everything else
+  // keeps the orthonormal frame about n / |n| (O(1e-7) apart).
+#if PGG_WOL_RAW_FRAME == 2
+  // (the two frames' local views differ in azimuth by ~1e-7 / |wo.xy|: only
+  // views within ~0.1 of n need the raw frame for 1e-6)
+  const V3<double> wn = fd.to_local(wd);
+  if (wn.x * wn.x + wn.y * wn.y >= 1e-2) {
+    p.wol = cvt<float>(wn);
+  } else
+#endif
+  {
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+    p.wol = cvt<float>(make_frame_fast(nd).to_local(wd));
+#else
+    p.wol = cvt<float>(make_frame(nd).to_local(wd));
+#endif
+  }
+#else
   p.wol = cvt<float>(fd.to_local(wd));
+#endif
   p.co_pos = radd(radd(rmul(wd.x, nd.x), rmul(wd.y, nd.y)), rmul(wd.z, nd.z)) > 0.0;
   p.om_nn = (float)(1.0 - nn);
   return p;
