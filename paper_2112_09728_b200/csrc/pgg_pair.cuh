@@ -132,12 +132,12 @@ PGG_PI void em_accumulate2(const EmSetup& S, const float4& vy0, const float4& vy
                 fma2(om.x, fr.n.x, fma2(om.y, fr.n.y, om.z * fr.n.z))};
   const float dz0 = lo(dl.z), dz1 = hi(dl.z);
   if (ok0 && (lo(dist2) < 1e-12f || fabsf(dz0) < 1e-6f)) {
-    ok0 = record_valid_d(vy0.x, vy0.y, vy0.z, S.x, n_raw());
+    ok0 = record_cos_d(vy0.x, vy0.y, vy0.z, S.x, n_raw()) > 0.0f;
   } else {
     ok0 = ok0 && dz0 > 1e-9f;
   }
   if (ok1 && (hi(dist2) < 1e-12f || fabsf(dz1) < 1e-6f)) {
-    ok1 = record_valid_d(vy1.x, vy1.y, vy1.z, S.x, n_raw());
+    ok1 = record_cos_d(vy1.x, vy1.y, vy1.z, S.x, n_raw()) > 0.0f;
   } else {
     ok1 = ok1 && dz1 > 1e-9f;
   }

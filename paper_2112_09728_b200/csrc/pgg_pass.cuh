@@ -675,13 +675,37 @@ PGG_HD uint32_t pcg_out(uint64_t old) {
   return (xs >> rot) | (xs << ((32u - rot) & 31u));
 }
 
-// validity thresholds dist > 1e-9 and cos > 1e-9 decided in float64
-PGG_COLD bool record_valid_d(float yx, float yy, float yz, V3<float> x, V3<float> n) {
+// validity thresholds dist > 1e-9 and cos > 1e-9 decided in float64:
+// returns the float64 receiver cosine (the reference's cos_r,
+// guide_buffers.py:186-196) rounded to float32 for a valid record, -1
+// otherwise.  Near the horizon the float32 cosine of the loop is ~6e-8
+// absolute off (the position difference is rounded): a 0.6 % weight error
+// at cos = 1e-5, which moved one 4K pixel's Gamma by 8e-4 relative where that
+// record held the responsibility mass.
+#ifndef PGG_GRAZE
+#define PGG_GRAZE 1e-4f  // |cos| below which a record's cosine is re-evaluated in float64
+#endif
+#ifndef PGG_GRAZE_FIX
+#define PGG_GRAZE_FIX 1
+#endif
+PGG_HD float record_cos_d_inl(float yx, float yy, float yz, V3<float> x, V3<float> n) {
+  const V3<double> dd = cvt<double>(v3(yx, yy, yz)) - cvt<double>(x);
+  const double dd2 = dot(dd, dd);
+#if PGG_FAST_F64 && defined(__CUDA_ARCH__)
+  const double c = dot(dd, cvt<double>(n)) * d_rsqrt(fmax(dd2, 1e-300));
+#else
+  const double c = dot(dd, cvt<double>(n)) / sqrt(fmax(dd2, 1e-300));
+#endif
+  return (dd2 > 1e-18 && c > 1e-9) ? (float)c : -1.0f;
+}
+PGG_COLD float record_cos_d(float yx, float yy, float yz, V3<float> x, V3<float> n) {
   const V3<double> dd = cvt<double>(v3(yx, yy, yz)) - cvt<double>(x);
   const double distd = sqrt(dot(dd, dd));
   const V3<double> omd = dd * (1.0 / fmax(distd, 1e-12));
-  return distd > 1e-9 && dot(omd, cvt<double>(n)) > 1e-9;
+  const double c = dot(omd, cvt<double>(n));
+  return (distd > 1e-9 && c > 1e-9) ? (float)c : -1.0f;
 }
+
 
 // VPL accessors for the record loop: straight from global memory (L2), or
 // from a shared-memory tile (own 32 x 8 block + EM halo) staged by TMA.
@@ -766,8 +790,10 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
   const V3<float> om = d * rinv;
   const V3<float> dl = S.fr.to_local(om);
-  if (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f) {
-    if (!record_valid_d(vy.x, vy.y, vy.z, S.x, S.n_raw)) return false;
+  float cr = dl.z;
+  if (dist2 < 1e-12f || fabsf(dl.z) < PGG_GRAZE) {
+    cr = record_cos_d(vy.x, vy.y, vy.z, S.x, S.n_raw);
+    if (!(cr > 0.0f)) return false;
   } else if (!(dl.z > 1e-9f)) {
     return false;
   }
@@ -775,7 +801,6 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
   o.w = 0.0f;
   o.r = 0.0f;
   if (!co_pos && !kAll) return true;  // f = 0 and brdf_pdf = 0: zero weight
-  const float cr = dl.z;
   float bp = 0.0f;
   if (co_pos) {
     const float4 lv = V.get_L(cx, cy);
@@ -826,12 +851,29 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
   const float rinv = r_rsqrt(fmaxf(dist2, 1e-24f));
 #endif
   const V3<float> dl = S.fr.to_local(d * rinv);
+#if PGG_GRAZE_FIX
+  // near-horizon records: the receiver cosine in float64 (weight and
+  // Lambert pdf are linear in it; float32 is ~6e-8 absolute off)
+  float cz = dl.z;
+  if (ok && (dist2 < 1e-12f || fabsf(dl.z) < PGG_GRAZE)) {
+#if PGG_GRAZE_FIX == 2
+    cz = record_cos_d_inl(vy.x, vy.y, vy.z, S.x, n_raw());
+#else
+    cz = record_cos_d(vy.x, vy.y, vy.z, S.x, n_raw());  // stored normal, reloaded: not live in the loop
+#endif
+    ok = cz > 0.0f;
+  } else {
+    ok = ok && dl.z > 1e-9f;
+  }
+  const float cr = fmaxf(cz, 0.0f);
+#else
   if (ok && (dist2 < 1e-12f || fabsf(dl.z) < 1e-6f)) {
-    ok = record_valid_d(vy.x, vy.y, vy.z, S.x, n_raw());  // stored normal, reloaded: not live in the loop
+    ok = record_cos_d(vy.x, vy.y, vy.z, S.x, n_raw()) > 0.0f;  // stored normal, reloaded: not live in the loop
   } else {
     ok = ok && dl.z > 1e-9f;
   }
   const float cr = fmaxf(dl.z, 0.0f);
+#endif
   const float4 lv = V.L_at(idx);
   // Lambert (scene.py:269, 296)
   float bp = cr * K<float>::inv_pi;

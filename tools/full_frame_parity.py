@@ -43,6 +43,14 @@ def work(rows):
                strat_bad=int(np.count_nonzero(sm["strategy"] != osmp["strategy"])),
                valid_bad=int(np.count_nonzero(sm["valid"] != osmp["valid"])),
                dir_err=direrr, pdf_rel=prel, worst=[])
+    gr = out["gam_rel"]
+    out["worst_gamma"] = []
+    for i in np.argsort(gr.ravel())[::-1][:3]:
+        yy, xx, c = np.unravel_index(int(i), gr.shape)
+        out["worst_gamma"].append(dict(y=r0 + int(yy), x=int(xx), ch=int(c), rel=float(gr[yy, xx, c]),
+                                       got=float(gam[yy, xx, c]), ref=float(otr[yy, xx, c]),
+                                       gin=g["gin"][r0 + yy, xx].tolist(), got_px=gam[yy, xx].tolist(),
+                                       ref_px=otr[yy, xx].tolist()))
     for i in np.argsort(direrr.ravel())[::-1][:3]:
         p, s = divmod(int(i), spp)
         out["worst"].append(dict(y=r0 + p // w, x=p % w, lane=s, dir_err=float(direrr.ravel()[i]),
@@ -83,7 +91,8 @@ def run(w, h, spp, F, seed=0, chunk=24):
                valid_mismatches=sum(x["valid_bad"] for x in res),
                dir_abs_max=float(de.max()), dir_lanes_gt_1e5=int(np.count_nonzero(de > 1e-5)),
                dir_lanes_gt_3e6=int(np.count_nonzero(de > 3e-6)),
-               pdf_rel_p9999=float(np.percentile(pr, 99.99)), pdf_rel_max=float(pr.max()), worst_dirs=worst)
+               pdf_rel_p9999=float(np.percentile(pr, 99.99)), pdf_rel_max=float(pr.max()), worst_dirs=worst,
+               worst_gamma=sorted([wg for x in res for wg in x["worst_gamma"]], key=lambda d: -d["rel"])[:8])
     print(json.dumps(rec), flush=True)
     return rec
 
