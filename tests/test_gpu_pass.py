@@ -289,3 +289,19 @@ def test_4k_4spp_vs_oracle(cuda_dev):
         assert osmp["wi"].shape == sb["wi"].shape
         check_samples(sb, osmp["wi"], osmp["pdf"], osmp["strategy"], osmp["valid"])
         assert sb["strategy"].any() and not sb["strategy"].all()
+
+def test_1080p_whole_frame_vs_oracle(cuda_dev):
+    """Every pixel and lane of the benchmarked 1080p frame (bench sequence
+    frame 12: Gamma trained over 12 GPU frames, k up to 12, disocclusions)
+    against the CPU oracle (row chunks in a fork pool), SURVEY 8a
+    single-kernel policy over the whole frame: Gamma p99.99 <= 1e-4, max <=
+    1e-3, k exact; strategy and validity exact; directions <= 1e-5; pdf
+    p99.99 <= 1e-4, max <= 1e-3.  tools/full_frame_parity.py runs the same
+    for frame 4 and a 4K 4 spp frame (profiles/r2_full_frame_parity.json)."""
+    from helpers.full_frame import run
+    rec = run(1920, 1080, 1, 13, verbose=False)
+    summary = {k: v for k, v in rec.items() if not k.startswith("worst")}
+    assert rec["k_mismatches"] == 0 and rec["strategy_mismatches"] == 0 and rec["valid_mismatches"] == 0, summary
+    assert rec["gamma_rel_p9999"] <= 1e-4 and rec["gamma_rel_max"] <= 1e-3, summary
+    assert rec["dir_abs_max"] <= 1e-5, (summary, rec["worst_dirs"][:2])
+    assert rec["pdf_rel_p9999"] <= 1e-4 and rec["pdf_rel_max"] <= 1e-3, summary
