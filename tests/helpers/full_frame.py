@@ -49,7 +49,7 @@ def work(rows):
     g = G
     w, spp = g["w"], g["spp"]
     _, osmp, otr = O.guiding_frame(g["gin"], g["gpn"], g["gcn"], g["vcn"], g["seed"], g["frame"], spp=spp,
-                                   rows=(r0, r1))
+                                   kmax=g["kmax"], radius=g["radius"], rows=(r0, r1))
     band = slice(r0 * w, r1 * w)
     gam = g["got"][r0:r1]
     sm = {k: v[band] for k, v in g["smp"].items()}
@@ -85,10 +85,10 @@ def work(rows):
     return out
 
 
-def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True):
+def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True, k_max=64, radius=10.0):
     dev = torch.device("cuda:0")
     frames = list(synth.sequence(w, h, F, seed=seed, device=dev))
-    cfg = PassConfig(seed=seed, spp=spp)
+    cfg = PassConfig(seed=seed, spp=spp, k_max=k_max, neighbor_radius=radius)
     sess = GuidingSession(w, h, cfg, device=dev)
     for f in range(F - 1):
         g, v = frames[f]
@@ -98,7 +98,7 @@ def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True):
     r = run_pass(cfg, F - 1, GBufferPlanes.from_ref(gc, device=dev), GammaPlanes.from_aos(gin, dev),
                  prev=GBufferPlanes.from_ref(gp, device=dev), vpl=VplPlanes.from_ref(vc, device=dev))
     G.clear()
-    G.update(w=w, spp=spp, seed=seed, frame=F - 1, gin=gin, gpn=_ns(gp), gcn=_ns(gc), vcn=_ns(vc),
+    G.update(w=w, spp=spp, seed=seed, frame=F - 1, kmax=k_max, radius=radius, gin=gin, gpn=_ns(gp), gcn=_ns(gc), vcn=_ns(vc),
              got=r.gamma.to_aos().cpu().numpy(), smp=_samples(r, w * h, spp))
     del frames, sess, r
     torch.cuda.empty_cache()
@@ -110,7 +110,7 @@ def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True):
     de = np.concatenate([x["dir_err"] for x in res])
     pr = np.concatenate([x["pdf_rel"] for x in res])
     worst = sorted([wl for x in res for wl in x["worst"]], key=lambda d: -d["dir_err"])[:8]
-    rec = dict(config=f"{w}x{h} {spp} spp frame {F - 1}", pixels=w * h, lanes=w * h * spp,
+    rec = dict(config=f"{w}x{h} {spp} spp frame {F - 1}, k_max {k_max}, radius {radius}", pixels=w * h, lanes=w * h * spp,
                oracle_seconds=round(time.time() - t0, 1),
                gamma_rel_p9999=float(np.percentile(gam, 99.99)), gamma_rel_max=float(gam.max()),
                gamma_channels_gt_1e4=int(np.count_nonzero(gam > 1e-4)),

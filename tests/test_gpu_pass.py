@@ -305,3 +305,18 @@ def test_1080p_whole_frame_vs_oracle(cuda_dev):
     assert rec["gamma_rel_p9999"] <= 1e-4 and rec["gamma_rel_max"] <= 1e-3, summary
     assert rec["dir_abs_max"] <= 1e-5, (summary, rec["worst_dirs"][:2])
     assert rec["pdf_rel_p9999"] <= 1e-4 and rec["pdf_rel_max"] <= 1e-3, summary
+
+
+@pytest.mark.parametrize("spp,k_max,radius", [(2, 32, 7.3), (3, 16, 12.0)])
+def test_whole_frame_other_configs(cuda_dev, spp, k_max, radius):
+    """Whole-frame parity at non-default pass parameters (640x360 bench
+    sequence, frame 8): EM radius 7.3 / 12 (the shared tile's halo at its
+    largest), k_max 32 / 16 (budgets reach their minimum of 5 sooner), 2 / 3
+    spp (lane keys pix * spp + s) -- same policy as the 1080p test."""
+    from helpers.full_frame import run
+    rec = run(640, 360, spp, 9, verbose=False, k_max=k_max, radius=radius, chunk=8)
+    summary = {k: v for k, v in rec.items() if not k.startswith("worst")}
+    assert rec["k_mismatches"] == 0 and rec["strategy_mismatches"] == 0 and rec["valid_mismatches"] == 0, summary
+    assert rec["gamma_rel_p9999"] <= 1e-4 and rec["gamma_rel_max"] <= 1e-3, summary
+    assert rec["dir_abs_max"] <= 1e-5, (summary, rec["worst_dirs"][:2])
+    assert rec["pdf_rel_p9999"] <= 1e-4 and rec["pdf_rel_max"] <= 1e-3, summary
