@@ -11,6 +11,7 @@ import multiprocessing as mp
 import os
 import sys
 import time
+import warnings
 
 import numpy as np
 import torch
@@ -104,8 +105,11 @@ def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True, k_max=64, radi
     torch.cuda.empty_cache()
     t0 = time.time()
     bands = [(a, min(h, a + chunk)) for a in range(0, h, chunk)]
-    with mp.get_context("fork").Pool(procs or os.cpu_count()) as pool:
-        res = pool.map(work, bands)
+    with warnings.catch_warnings():
+        # the children run numpy only (no CUDA, no locks of the parent's threads)
+        warnings.filterwarnings("ignore", message=".*use of fork\\(\\) may lead to deadlocks.*")
+        with mp.get_context("fork").Pool(procs or os.cpu_count()) as pool:
+            res = pool.map(work, bands)
     gam = np.concatenate([x["gam_rel"] for x in res])
     de = np.concatenate([x["dir_err"] for x in res])
     pr = np.concatenate([x["pdf_rel"] for x in res])
