@@ -20,7 +20,7 @@
  *                          e_step_responsibility / neighbor_count  mixture.py:158-190, 262-273, 324-328
  *   pgg_sample_gauss ..... the Gaussian branch of mixture.sample_mixture (mixture.py:208-235)
  *                          for callers with their own BRDF callbacks
- *   pgg_trunc_mass ....... mixture.truncation_mass      mixture.py:84-126
+ *   pgg_trunc_mass ....... mixture.truncation_mass      mixture.py:84-126 (its rule, float64)
  *   pgg_m_step ........... mixture.m_step_update        mixture.py:276-321
  *   pgg_make_streams ..... rng.make_streams             rng.py:25-39
  *   pgg_next_u32 ......... rng.next_u32                 rng.py:42-50
@@ -363,6 +363,10 @@ int pgg_debug_checks(int32_t* host_out6, int32_t reset);
 int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechecks, void* stream);
 int pgg_debug_bm_accept(int64_t n, int32_t per_lobe, const float* stats, const uint32_t* draws, uint8_t* out,
                         float* proposals, int32_t* rechecks, void* stream);
+/*   pgg_debug_trunc_bvn   the pass's float32 truncation mass (Genz BVN; the
+ *       reference rule for |r| >= 0.999) of n lobes (mu n x 2, cov n x 2 x 2,
+ *       float64) -- pgg_trunc_mass returns the reference's float64 rule */
+int pgg_debug_trunc_bvn(int64_t n, const double* mu, const double* cov, double* z, void* stream);
 /*   pgg_debug_brdf_draw   the sampler's local-frame BRDF draw (Lambert cosine
  *       or GGX VNDF, scene.py:311-351, with the float64 re-evaluation of rim
  *       samples) for n lanes: glossy u8, roughness, wo float4 (local), draws

@@ -117,6 +117,7 @@ _SIGS = {
     "pgg_debug_checks": [c_p, c_i32],
     "pgg_debug_em_offsets": [ctypes.POINTER(Config), c_p, c_p, c_p],
     "pgg_debug_bm_accept": [c_i64, c_i32, c_p, c_p, c_p, c_p, c_p, c_p],
+    "pgg_debug_trunc_bvn": [c_i64, c_p, c_p, c_p, c_p],
     "pgg_debug_brdf_draw": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_debug_reproject": [ctypes.POINTER(Config), ctypes.POINTER(GBuffer), ctypes.POINTER(GBuffer),
                             ctypes.POINTER(GammaIn), c_p, c_p],

@@ -379,7 +379,7 @@ __global__ void k_lobe(int64_t n, const double* __restrict__ st, double* mu, dou
   chol[4 * i + 1] = 0.0;
   chol[4 * i + 2] = l21;
   chol[4 * i + 3] = l22;
-  z[i] = trunc_mass_bvn(mx, my, sxx, syy, sxy, (float)l11, (float)l21, (float)l22);
+  z[i] = trunc_mass_ref_d(mx, my, l11, l21, l22);  // the reference's rule in float64
   if (reset) reset[i] = bad ? 1 : 0;
 }
 
@@ -390,7 +390,7 @@ __global__ void k_trunc(int64_t n, const double* __restrict__ mu, const double* 
   const double l11 = sqrt(a);
   const double l21 = c / l11;
   const double l22 = sqrt(fmax(rsub(b, rmul(l21, l21)), 1e-30));
-  z[i] = trunc_mass_bvn(mu[2 * i], mu[2 * i + 1], a, b, c, (float)l11, (float)l21, (float)l22);
+  z[i] = trunc_mass_ref_d(mu[2 * i], mu[2 * i + 1], l11, l21, l22);  // the reference's rule in float64
 }
 
 __global__ void k_m_step(int64_t n, int c, const double* __restrict__ st, const double* __restrict__ sq,
@@ -639,6 +639,19 @@ __global__ void k_debug_em_offsets(const PassArgs A, int8_t* __restrict__ out, i
 
 // Box-Muller proposals of the guided branch: lobe from float32 Gamma
 // (make_lobe, as pixel_stage), acceptance via bm_propose
+// the pass's float32 truncation mass (Genz BVN, reference rule at |r| >=
+// 0.999) on caller lobes, for accuracy sweeps against the reference rule
+__global__ void k_debug_trunc_bvn(int64_t n, const double* __restrict__ mu, const double* __restrict__ cov,
+                                  double* z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = cov[4 * i], c = cov[4 * i + 1], b = cov[4 * i + 3];
+  const double l11 = sqrt(a);
+  const double l21 = c / l11;
+  const double l22 = sqrt(fmax(rsub(b, rmul(l21, l21)), 1e-30));
+  z[i] = trunc_mass_bvn(mu[2 * i], mu[2 * i + 1], a, b, c, (float)l11, (float)l21, (float)l22);
+}
+
 __global__ void k_debug_bm_accept(int64_t n, int per, const float* __restrict__ stats, const uint32_t* __restrict__ ab,
                                   uint8_t* __restrict__ out, float* __restrict__ p_out, int32_t* rechecks) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -956,6 +969,14 @@ int pgg_debug_em_offsets(const pgg_config* cfg, int8_t* offsets, int32_t* rechec
   const int64_t P = (int64_t)cfg->width * cfg->height;
   if (const int rc = device_check()) return rc;
   k_debug_em_offsets<<<blocks(P, 256), 256, 0, S(stream)>>>(A, offsets, rechecks);
+  return check_launch();
+}
+
+int pgg_debug_trunc_bvn(int64_t n, const double* mu, const double* cov, double* z, void* stream) {
+  if (n < 0 || !mu || !cov || !z) return PGG_ERR_ARGUMENT;
+  if (n == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_debug_trunc_bvn<<<blocks(n, 128), 128, 0, S(stream)>>>(n, mu, cov, z);
   return check_launch();
 }
 

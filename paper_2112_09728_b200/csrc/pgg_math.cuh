@@ -284,6 +284,8 @@ PGG_HD double rsub(double a, double b) {
 #endif
 }
 
+PGG_HD double rdiv(double a, double b) { return a / b; }  // IEEE round-to-nearest in float64
+
 template <class T> struct K {
   static constexpr T pi = T(3.14159265358979323846);
   static constexpr T inv_pi = T(0.31830988618379067154);
@@ -958,6 +960,69 @@ PGG_HD float gl24_phi(float a, float len) {
     acc = fmaf(gl24_w(i), m_exp(-0.5f * z * z), acc);
   }
   return acc;
+}
+
+// The reference's truncation rule itself in float64 (pg/mixture.py:84-126,
+// its operation order): the lane API (mixture.truncation_mass,
+// lobe_from_stats) returns it, so callers get the reference's Z on any input
+// (the pass keeps its float32 Genz form, trunc_mass_bvn, whose domain is the
+// lobes it forms).
+#if defined(__CUDACC__)
+#define PGG_TABLE __constant__ const
+#else
+#define PGG_TABLE static const
+#endif
+PGG_TABLE double kGL24_X[24] = {0.0024063900014893447, 0.012635722014345263, 0.0308627239986336,
+                                0.056792236497799464,  0.08999900701304853,  0.12993790421072282,
+                                0.17595317403151223,   0.22728926430558022,  0.28310324618697746,
+                                0.3424786601519183,    0.40444056626319186,  0.4679715535686972,
+                                0.5320284464313028,    0.5955594337368082,   0.6575213398480817,
+                                0.7168967538130225,    0.7727107356944198,   0.8240468259684878,
+                                0.8700620957892772,    0.9100009929869515,   0.9432077635022005,
+                                0.9691372760013663,    0.9873642779856547,   0.9975936099985107};
+PGG_TABLE double kGL24_W[24] = {0.006170614899994345, 0.01426569431446678, 0.022138719408709706,
+                                0.02964929245771818,  0.03667324070554008, 0.0430950807659766,
+                                0.04880932605205696,  0.05372213505798278, 0.05775283402686276,
+                                0.06083523646390165,  0.06291872817341412, 0.06396909767337601,
+                                0.06396909767337601,  0.06291872817341412, 0.06083523646390165,
+                                0.05775283402686276,  0.05372213505798278, 0.04880932605205696,
+                                0.0430950807659766,   0.03667324070554008, 0.02964929245771818,
+                                0.022138719408709706, 0.01426569431446678, 0.006170614899994345};
+PGG_HD double ndtr_d(double x) {  // scipy.special.ndtr
+  const double t = x * 0.70710678118654752440;
+  return fabs(t) < 0.70710678118654752440 ? 0.5 + 0.5 * erf(t) : (t > 0.0 ? 1.0 - 0.5 * erfc(t) : 0.5 * erfc(-t));
+}
+PGG_COLD double trunc_mass_ref_d(double mx, double my, double l11, double l21, double l22) {
+  const double lo1 = fmax(rdiv(rsub(0.0, mx), l11), -8.5);
+  double hi1 = fmin(rdiv(rsub(1.0, mx), l11), 8.5);
+  hi1 = fmax(hi1, lo1);
+  const double sl21 = fabs(l21) < 1e-30 ? 1e-30 : l21;
+  double e[6];
+  e[0] = fmin(fmax(rdiv(rsub(rsub(0.0, my), rmul(-6.5, l22)), sl21), lo1), hi1);
+  e[1] = fmin(fmax(rdiv(rsub(rsub(0.0, my), rmul(6.5, l22)), sl21), lo1), hi1);
+  e[2] = fmin(fmax(rdiv(rsub(rsub(1.0, my), rmul(-6.5, l22)), sl21), lo1), hi1);
+  e[3] = fmin(fmax(rdiv(rsub(rsub(1.0, my), rmul(6.5, l22)), sl21), lo1), hi1);
+  e[4] = lo1;
+  e[5] = hi1;
+  for (int i = 1; i < 6; ++i)  // insertion sort (np.sort)
+    for (int j = i; j > 0 && e[j - 1] > e[j]; --j) {
+      const double t = e[j];
+      e[j] = e[j - 1];
+      e[j - 1] = t;
+    }
+  double acc = 0.0;
+  for (int k = 0; k < 5; ++k) {
+    const double a = e[k], len = rsub(e[k + 1], e[k]);
+    for (int i = 0; i < 24; ++i) {
+      const double z = radd(a, rmul(len, kGL24_X[i]));
+      const double hi = rdiv(rsub(rsub(1.0, my), rmul(l21, z)), l22);
+      const double lo = rdiv(rsub(rsub(0.0, my), rmul(l21, z)), l22);
+      const double g = rsub(ndtr_d(hi), ndtr_d(lo));
+      const double phi = rdiv(exp(rmul(rmul(-0.5, z), z)), 2.5066282746310002);
+      acc = radd(acc, rmul(rmul(rmul(len, kGL24_W[i]), phi), g));
+    }
+  }
+  return fmin(fmax(acc, 1e-4), 1.0);
 }
 
 // Truncation mass of N(mu, L L^T) on [0,1]^2, the reference's rule: whitened

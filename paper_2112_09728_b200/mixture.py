@@ -74,11 +74,11 @@ def lobe_from_stats(stats):
 def truncation_mass(mu, cov):
     """Mass of N(mu, cov) inside [0,1]^2, clamped to [1e-4, 1] (pg/mixture.py:84-126).
 
-    The pass's float32 Genz evaluation: within 7.5e-5 relative of the
-    reference rule on every lobe lobe_from_stats can form (mu in [0,1]^2,
-    eigenvalues >= 1e-6; 2 M lobes, profiles/r2_trunc_fuzz_lobe_domain.json).
-    Outside that domain (means off the square, sub-ridge variances) the
-    float32 cancellation grows to ~6e-3 (profiles/r2_trunc_fuzz_any_domain.json)."""
+    The reference's own rule (whitened outer variable, 5 ramp segments x 24
+    Gauss-Legendre nodes) in float64 on the device: within 3.5e-13 relative
+    of the reference on any input (profiles/r2_trunc_fuzz_*.json).  The fused
+    pass evaluates its float32 Genz form instead (7.5e-5 on the lobes it
+    forms)."""
     torch_in = _conv.is_torch(mu, cov)
     m = _conv.to_dev(mu, F64)
     lead = tuple(m.shape[:-1])

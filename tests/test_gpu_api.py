@@ -43,7 +43,9 @@ def test_mixture_api(cuda_dev, kat):
     np.testing.assert_array_equal(lb.mu, kat["lobe_mu"])
     np.testing.assert_array_equal(lb.cov, kat["lobe_cov"])
     np.testing.assert_array_equal(lb.chol, kat["lobe_chol"])
-    assert gio.rel_err(lb.trunc_z, kat["lobe_z"]).max() <= 1e-4   # see test_hostcheck.test_lobe_trunc_mass
+    # the API evaluates the reference's own rule in float64 (the pass uses its
+    # float32 Genz form, test_hostcheck.test_lobe_trunc_mass / tools/trunc_fuzz.py)
+    assert gio.rel_err(lb.trunc_z, kat["lobe_z"]).max() <= 1e-12
     np.testing.assert_allclose(M.truncation_mass(kat["lobe_mu"], kat["lobe_cov"]), lb.trunc_z, rtol=0, atol=0)
     ref_lobe = O.lobe(st)
     ref_pdf = O.gauss_sq_pdf(SimpleNamespace(mu=ref_lobe.mu, l11=ref_lobe.l11, l21=ref_lobe.l21, l22=ref_lobe.l22,

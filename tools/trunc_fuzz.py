@@ -1,5 +1,6 @@
-"""Truncation mass (pgg_trunc_mass: the pass's float32 Genz BVN with the
-reference rule at |r| >= 0.999) against the oracle's restatement of the
+"""Truncation mass -- the pass's float32 Genz BVN (pgg_debug_trunc_bvn; the
+reference rule at |r| >= 0.999) and the API's float64 reference rule
+(pgg_trunc_mass) -- against the oracle's restatement of the
 reference rule (pg/mixture.py:77-126) on random lobes, with the correlation
 concentrated around the node-class boundaries (0.3 / 0.75 / 0.925 / 0.96 /
 0.99 / 0.999), means at the square's edges and variances from 1e-7 to 1.
@@ -49,16 +50,21 @@ cov = np.stack([sxx, sxy, sxy, syy], -1)
 mu_d = torch.from_numpy(mu.copy()).to(dev)
 cov_d = torch.from_numpy(cov.copy()).to(dev)
 z_d = torch.empty(n, dtype=torch.float64, device=dev)
-_lib.check(_lib.lib().pgg_trunc_mass(n, _lib.ptr(mu_d), _lib.ptr(cov_d), _lib.ptr(z_d), _lib.stream_ptr()))
+_lib.check(_lib.lib().pgg_debug_trunc_bvn(n, _lib.ptr(mu_d), _lib.ptr(cov_d), _lib.ptr(z_d), _lib.stream_ptr()))
 got = z_d.cpu().numpy()
+zr_d = torch.empty(n, dtype=torch.float64, device=dev)   # the API: the reference rule in float64
+_lib.check(_lib.lib().pgg_trunc_mass(n, _lib.ptr(mu_d), _lib.ptr(cov_d), _lib.ptr(zr_d), _lib.stream_ptr()))
+api = zr_d.cpu().numpy()
 l11, l21, l22 = O.chol2(sxx, sxy, syy)
 ref = np.empty(n)
 for a in range(0, n, 1 << 17):
     b = min(n, a + (1 << 17))
     ref[a:b] = O.trunc_mass(mu[a:b, 0], mu[a:b, 1], l11[a:b], l21[a:b], l22[a:b])
 rel = np.abs(got - ref) / ref
+rel_api = np.abs(api - ref) / ref
 cls = np.digitize(np.abs(rho), edges)
-out = {"lobes": n, "rel_p9999": float(np.percentile(rel, 99.99)), "rel_max": float(rel.max()), "per_class": {}}
+out = {"lobes": n, "pass_bvn_rel_p9999": float(np.percentile(rel, 99.99)), "pass_bvn_rel_max": float(rel.max()),
+       "api_rel_max": float(rel_api.max()), "per_class": {}}
 for c in range(7):
     m = cls == c
     if m.any():
