@@ -50,7 +50,7 @@ def work(rows):
     g = G
     w, spp = g["w"], g["spp"]
     _, osmp, otr = O.guiding_frame(g["gin"], g["gpn"], g["gcn"], g["vcn"], g["seed"], g["frame"], spp=spp,
-                                   kmax=g["kmax"], radius=g["radius"], rows=(r0, r1))
+                                   kmax=g["kmax"], radius=g["radius"], nee_draws=g.get("nee", 3), rows=(r0, r1))
     band = slice(r0 * w, r1 * w)
     gam = g["got"][r0:r1]
     sm = {k: v[band] for k, v in g["smp"].items()}
@@ -86,23 +86,13 @@ def work(rows):
     return out
 
 
-def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True, k_max=64, radius=10.0):
-    dev = torch.device("cuda:0")
-    frames = list(synth.sequence(w, h, F, seed=seed, device=dev))
-    cfg = PassConfig(seed=seed, spp=spp, k_max=k_max, neighbor_radius=radius)
-    sess = GuidingSession(w, h, cfg, device=dev)
-    for f in range(F - 1):
-        g, v = frames[f]
-        sess.step(GBufferPlanes.from_ref(g, device=dev), VplPlanes.from_ref(v, device=dev), f)
-    gin = sess.gamma.to_aos().cpu().numpy()
-    (gp, _), (gc, vc) = frames[F - 2], frames[F - 1]
-    r = run_pass(cfg, F - 1, GBufferPlanes.from_ref(gc, device=dev), GammaPlanes.from_aos(gin, dev),
-                 prev=GBufferPlanes.from_ref(gp, device=dev), vpl=VplPlanes.from_ref(vc, device=dev))
+def compare(gin, gpn, gcn, vcn, got, smp, w, h, spp, seed, frame, k_max=64, radius=10.0, chunk=24, procs=None,
+            label="", nee_draws=3):
+    """GPU outputs (Gamma' AoS `got`, samples dict `smp`) of one pass against
+    the oracle's guiding_frame on the same inputs, every row."""
     G.clear()
-    G.update(w=w, spp=spp, seed=seed, frame=F - 1, kmax=k_max, radius=radius, gin=gin, gpn=_ns(gp), gcn=_ns(gc), vcn=_ns(vc),
-             got=r.gamma.to_aos().cpu().numpy(), smp=_samples(r, w * h, spp))
-    del frames, sess, r
-    torch.cuda.empty_cache()
+    G.update(w=w, spp=spp, seed=seed, frame=frame, kmax=k_max, radius=radius, gin=gin, gpn=gpn, gcn=gcn, vcn=vcn,
+             got=got, smp=smp, nee=nee_draws)
     t0 = time.time()
     bands = [(a, min(h, a + chunk)) for a in range(0, h, chunk)]
     with warnings.catch_warnings():
@@ -114,17 +104,36 @@ def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True, k_max=64, radi
     de = np.concatenate([x["dir_err"] for x in res])
     pr = np.concatenate([x["pdf_rel"] for x in res])
     worst = sorted([wl for x in res for wl in x["worst"]], key=lambda d: -d["dir_err"])[:8]
-    rec = dict(config=f"{w}x{h} {spp} spp frame {F - 1}, k_max {k_max}, radius {radius}", pixels=w * h, lanes=w * h * spp,
-               oracle_seconds=round(time.time() - t0, 1),
-               gamma_rel_p9999=float(np.percentile(gam, 99.99)), gamma_rel_max=float(gam.max()),
-               gamma_channels_gt_1e4=int(np.count_nonzero(gam > 1e-4)),
-               k_mismatches=sum(x["k_bad"] for x in res), strategy_mismatches=sum(x["strat_bad"] for x in res),
-               valid_mismatches=sum(x["valid_bad"] for x in res),
-               dir_abs_max=float(de.max()), dir_lanes_gt_1e5=int(np.count_nonzero(de > 1e-5)),
-               dir_lanes_gt_3e6=int(np.count_nonzero(de > 3e-6)),
-               pdf_rel_p9999=float(np.percentile(pr, 99.99)), pdf_rel_max=float(pr.max()), worst_dirs=worst,
-               worst_pdf=sorted([wp for x in res for wp in x["worst_pdf"]], key=lambda d: -d["rel"])[:8],
-               worst_gamma=sorted([wg for x in res for wg in x["worst_gamma"]], key=lambda d: -d["rel"])[:8])
+    return dict(config=label or f"{w}x{h} {spp} spp frame {frame}, k_max {k_max}, radius {radius}", pixels=w * h,
+                lanes=w * h * spp, oracle_seconds=round(time.time() - t0, 1),
+                gamma_rel_p9999=float(np.percentile(gam, 99.99)), gamma_rel_max=float(gam.max()),
+                gamma_channels_gt_1e4=int(np.count_nonzero(gam > 1e-4)),
+                k_mismatches=sum(x["k_bad"] for x in res), strategy_mismatches=sum(x["strat_bad"] for x in res),
+                valid_mismatches=sum(x["valid_bad"] for x in res),
+                dir_abs_max=float(de.max()), dir_lanes_gt_1e5=int(np.count_nonzero(de > 1e-5)),
+                dir_lanes_gt_3e6=int(np.count_nonzero(de > 3e-6)),
+                pdf_rel_p9999=float(np.percentile(pr, 99.99)), pdf_rel_max=float(pr.max()), worst_dirs=worst,
+                worst_pdf=sorted([wp for x in res for wp in x["worst_pdf"]], key=lambda d: -d["rel"])[:8],
+                worst_gamma=sorted([wg for x in res for wg in x["worst_gamma"]], key=lambda d: -d["rel"])[:8])
+
+
+def run(w, h, spp, F, seed=0, chunk=24, procs=None, verbose=True, k_max=64, radius=10.0):
+    """The bench sequence's frame F - 1 (Gamma from F - 1 GPU frames)."""
+    dev = torch.device("cuda:0")
+    frames = list(synth.sequence(w, h, F, seed=seed, device=dev))
+    cfg = PassConfig(seed=seed, spp=spp, k_max=k_max, neighbor_radius=radius)
+    sess = GuidingSession(w, h, cfg, device=dev)
+    for f in range(F - 1):
+        g, v = frames[f]
+        sess.step(GBufferPlanes.from_ref(g, device=dev), VplPlanes.from_ref(v, device=dev), f)
+    gin = sess.gamma.to_aos().cpu().numpy()
+    (gp, _), (gc, vc) = frames[F - 2], frames[F - 1]
+    r = run_pass(cfg, F - 1, GBufferPlanes.from_ref(gc, device=dev), GammaPlanes.from_aos(gin, dev),
+                 prev=GBufferPlanes.from_ref(gp, device=dev), vpl=VplPlanes.from_ref(vc, device=dev))
+    args = (gin, _ns(gp), _ns(gc), _ns(vc), r.gamma.to_aos().cpu().numpy(), _samples(r, w * h, spp))
+    del frames, sess, r
+    torch.cuda.empty_cache()
+    rec = compare(*args, w, h, spp, seed, F - 1, k_max, radius, chunk, procs)
     if verbose:
         print(json.dumps(rec), flush=True)
     return rec

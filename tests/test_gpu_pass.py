@@ -320,3 +320,21 @@ def test_whole_frame_other_configs(cuda_dev, spp, k_max, radius):
     assert rec["gamma_rel_p9999"] <= 1e-4 and rec["gamma_rel_max"] <= 1e-3, summary
     assert rec["dir_abs_max"] <= 1e-5, (summary, rec["worst_dirs"][:2])
     assert rec["pdf_rel_p9999"] <= 1e-4 and rec["pdf_rel_max"] <= 1e-3, summary
+
+
+@pytest.mark.parametrize("name", ["glossy-box", "indirect-corridor"])
+def test_whole_frame_rendered_scene(cuda_dev, name):
+    """Whole-frame parity on RENDERED inputs (640x360): the GPU frame loop
+    runs 3 guided frames of a built-in scene, then frame 3's G-buffer, its
+    path-traced VPLs and the trained Gamma go to the fused pass and to the
+    oracle -- axis-aligned planar normals, glossy and diffuse materials,
+    emitters (NEE draws).  Same policy as the synthetic whole-frame tests
+    (tools/scene_parity.py runs the three scenes at 1080p,
+    profiles/r2_scene_parity_1080p.json)."""
+    from helpers.scene_frame import one
+    rec = one(name, F=4, w=640, h=360)
+    summary = {k: v for k, v in rec.items() if not k.startswith("worst")}
+    assert rec["k_mismatches"] == 0 and rec["strategy_mismatches"] == 0 and rec["valid_mismatches"] == 0, summary
+    assert rec["gamma_rel_p9999"] <= 1e-4 and rec["gamma_rel_max"] <= 1e-3, summary
+    assert rec["dir_abs_max"] <= 1e-5, summary
+    assert rec["pdf_rel_p9999"] <= 1e-4 and rec["pdf_rel_max"] <= 1e-3, summary
