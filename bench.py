@@ -861,20 +861,41 @@ def bench_e2e(args, frames, cfg, dev, world):
     # strategy: 26 B/px, pg/ptrace.py:67-73) and are packed into the kernel's
     # float4 planes on the device (pgg_pack_vpl); the G-buffer crosses in the
     # packed planes (65 B/px, no padding)
-    raw = [v for _, v in synth.sequence(W, H, nh, seed=cfg.seed, device=dev)]
+    raw = list(synth.sequence(W, H, nh, seed=cfg.seed, device=dev))
+    pin = lambda t, dt: t.to(dt).contiguous().cpu().pin_memory()  # noqa: E731
+    f32, u8 = torch.float32, torch.uint8
     for i in range(nh):
-        g, _ = frames[i]
-        v = raw[i]
-        host.append({k: getattr(g, k).cpu().pin_memory() for k in ("flags", "nd", "pr", "va", "am")} |
-                    {"v_valid": v["valid"].to(torch.uint8).cpu().pin_memory(),
-                     "v_y": v["y"].to(torch.float32).contiguous().cpu().pin_memory(),
-                     "v_rad": v["radiance"].to(torch.float32).contiguous().cpu().pin_memory(),
-                     "v_strat": v["strategy"].to(torch.uint8).cpu().pin_memory(), "cam": g.cam_origin})
+        g, v = raw[i]
+        # the reference GBuffer's own fields (float32) with its material ids:
+        # kind / albedo / roughness come from the scene's material table on
+        # the device (pgg_pack_gbuffer_mat, 54 B/px instead of 65 B/px planes)
+        host.append({"g_valid": pin(g["valid"], u8), "g_pos": pin(g["pos"], f32), "g_nrm": pin(g["normal"], f32),
+                     "g_depth": pin(g["depth"], f32), "g_mat": pin(g["mat"], torch.int32),
+                     "g_view": pin(g["view"], f32), "g_motion": pin(g["motion"], f32),
+                     "g_hist": pin(g["has_history"], u8),
+                     "v_valid": pin(v["valid"], u8), "v_y": pin(v["y"], f32), "v_rad": pin(v["radiance"], f32),
+                     "v_strat": pin(v["strategy"], u8), "cam": frames[i][0].cam_origin})
     del raw
+    mkind, mrough, malb = (t.contiguous() for t in synth.materials(cfg.seed, dev))
+    mkind = mkind.to(torch.int32)
+    gkeys = ("g_valid", "g_pos", "g_nrm", "g_depth", "g_mat", "g_view", "g_motion", "g_hist")
+    vkeys = ("v_valid", "v_y", "v_rad", "v_strat")
     gbs = [GBufferPlanes.empty(H, W, dev) for _ in range(3)]        # cur / prev / next
     vps = [VplPlanes(torch.empty(H, W, 4, device=dev), torch.empty(H, W, 4, device=dev)) for _ in range(2)]
-    vraw = [{k: torch.empty_like(host[0][k], device=dev) for k in ("v_valid", "v_y", "v_rad", "v_strat")}
-            for _ in range(2)]
+    vraw = [{k: torch.empty_like(host[0][k], device=dev) for k in gkeys + vkeys} for _ in range(2)]
+    # the device packing reproduces the planes the pass benchmark runs on, bit for bit
+    chk = vraw[0]
+    for k in gkeys:
+        chk[k].copy_(host[0][k])
+    gchk = GBufferPlanes.empty(H, W, dev)
+    _lib.check(_lib.lib().pgg_pack_gbuffer_mat(
+        H * W, *[_lib.ptr(chk[k]) for k in gkeys[:5]], int(mkind.numel()), _lib.ptr(mkind), _lib.ptr(malb),
+        _lib.ptr(mrough), *[_lib.ptr(chk[k]) for k in gkeys[5:]], _lib.ptr(gchk.flags), _lib.ptr(gchk.nd),
+        _lib.ptr(gchk.pr), _lib.ptr(gchk.va), _lib.ptr(gchk.am), _lib.stream_ptr()))
+    g0 = frames[0][0]
+    if not all(torch.equal(getattr(gchk, k), getattr(g0, k)) for k in ("flags", "nd", "pr", "va", "am")):
+        raise RuntimeError("pgg_pack_gbuffer_mat planes differ from the benchmark's G-buffer planes")
+    del gchk
     gam = [GammaPlanes.fresh(H, W, dev), GammaPlanes.empty(H, W, dev)]
     smps = [SamplePlanes.empty(H, W, args.spp, dev) for _ in range(2)]
     outs = [torch.empty(H, W, 8, dtype=torch.float32, device=dev) for _ in range(2)]
@@ -898,8 +919,6 @@ def bench_e2e(args, frames, cfg, dev, world):
         with torch.cuda.stream(s_in):
             if i >= 2:
                 s_in.wait_event(cmp_done[(i - 2) % 3])    # slot last read by pass i-1 (as prev) / i-2
-            for k in ("flags", "nd", "pr", "va", "am"):
-                getattr(cur, k).copy_(hsrc[k], non_blocking=True)
             for k, t in vraw[i % 2].items():
                 t.copy_(hsrc[k], non_blocking=True)
             in_done[i % 3].record(s_in)
@@ -911,6 +930,10 @@ def bench_e2e(args, frames, cfg, dev, world):
                 s_cmp.wait_event(out_done[o])
             g_in, g_out = gam[st["g"]], gam[1 - st["g"]]
             r = vraw[i % 2]
+            _lib.check(_lib.lib().pgg_pack_gbuffer_mat(
+                H * W, *[_lib.ptr(r[k]) for k in gkeys[:5]], int(mkind.numel()), _lib.ptr(mkind), _lib.ptr(malb),
+                _lib.ptr(mrough), *[_lib.ptr(r[k]) for k in gkeys[5:]], _lib.ptr(cur.flags), _lib.ptr(cur.nd),
+                _lib.ptr(cur.pr), _lib.ptr(cur.va), _lib.ptr(cur.am), _lib.stream_ptr(s_cmp)))
             _lib.check(_lib.lib().pgg_pack_vpl(H * W, _lib.ptr(r["v_valid"]), _lib.ptr(r["v_y"]),
                                                _lib.ptr(r["v_rad"]), _lib.ptr(r["v_strat"]), _lib.ptr(vp.y),
                                                _lib.ptr(vp.L), _lib.stream_ptr(s_cmp)))
@@ -948,9 +971,9 @@ def bench_e2e(args, frames, cfg, dev, world):
         ms = float(t.item())
     return {"value": world * W * H / (ms * 1e-3) / 1e6, "unit": "Mpixels/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
-            "path": "pinned host: G-buffer planes + the reference's VplBuffer fields -> H2D -> pgg_pack_vpl -> "
-                    "pgg_guiding_pass -> pgg_gamma_join + samples -> D2H, 3 streams (copy-in / pass / copy-out) "
-                    "overlapping adjacent frames"}
+            "path": "pinned host: the reference's GBuffer fields (float32, material ids) + VplBuffer fields -> "
+                    "H2D -> pgg_pack_gbuffer_mat + pgg_pack_vpl -> pgg_guiding_pass -> pgg_gamma_join + samples -> "
+                    "D2H, 3 streams (copy-in / pass / copy-out) overlapping adjacent frames"}
 
 
 def main():

@@ -25,7 +25,8 @@
  *   pgg_make_streams ..... rng.make_streams             rng.py:25-39
  *   pgg_next_u32 ......... rng.next_u32                 rng.py:42-50
  *   pgg_frame_key ........ the lane-independent prefix of rng.make_streams
- *   pgg_pack_* / pgg_gamma_* layout conversion at the API edge
+ *   pgg_pack_* / pgg_gamma_* layout conversion at the API edge (pgg_pack_gbuffer_mat: from
+ *                          material ids + the scene's table)
  *
  * The render pass that feeds it:
  *   pgg_gbuffer_pass ..... ptrace.gbuffer_pass          ptrace.py:97-129
@@ -204,6 +205,16 @@ int pgg_pack_gbuffer(int64_t p, const uint8_t* valid, const float* pos, const fl
                      const float* depth, const int32_t* kind, const float* albedo, const float* rough,
                      const float* view, const float* motion, const uint8_t* has_history, uint8_t* flags,
                      float* nd, float* pr, float* va, float* am, void* stream);
+
+/* The same planes from the G-buffer's material ids (int32, -1 = miss) and the
+ * scene's material table (n_mat kinds, albedo rgb, roughness; the lookups of
+ * ptrace.gbuffer_pass, ptrace.py:97-129) instead of per-pixel kind / albedo
+ * / roughness: 16 B/px less to upload.  Bitwise the same planes. */
+int pgg_pack_gbuffer_mat(int64_t p, const uint8_t* valid, const float* pos, const float* normal,
+                         const float* depth, const int32_t* mat, int32_t n_mat, const int32_t* mat_kind,
+                         const float* mat_albedo, const float* mat_rough, const float* view, const float* motion,
+                         const uint8_t* has_history, uint8_t* flags, float* nd, float* pr, float* va, float* am,
+                         void* stream);
 
 /* Pack VplBuffer fields (valid u8, y f32 x3, radiance f32 x3, strategy u8). */
 int pgg_pack_vpl(int64_t p, const uint8_t* valid, const float* y, const float* radiance,

@@ -96,6 +96,8 @@ _SIGS = {
     "pgg_make_streams": [c_u64, c_i64, c_p, c_p, c_p],
     "pgg_next_u32": [c_i64, c_p, c_p, c_p],
     "pgg_pack_gbuffer": [c_i64] + [c_p] * 15 + [c_p],
+    "pgg_pack_gbuffer_mat": [c_i64, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
+                             c_p, c_p, c_p],
     "pgg_pack_vpl": [c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "pgg_gamma_split": [c_i64, c_p, c_p, c_p, c_p],
     "pgg_gamma_join": [c_i64, c_p, c_p, c_p, c_p],

@@ -458,6 +458,34 @@ __global__ void k_pack_gbuffer(int64_t p, const uint8_t* __restrict__ valid, con
   am[i] = f4(alb[3 * i + 1], alb[3 * i + 2], motion ? motion[2 * i] : 0.f, motion ? motion[2 * i + 1] : 0.f);
 }
 
+// the same planes from the material ids the reference's G-buffer carries
+// (pg/ptrace.py:97-129 looks kind / albedo / roughness up per material;
+// mat -1 = miss -> zeros), with the scene's material table: 16 B/px fewer
+// to move than per-pixel albedo / roughness / kind
+__global__ void k_pack_gbuffer_mat(int64_t p, const uint8_t* __restrict__ valid, const float* __restrict__ pos,
+                                   const float* __restrict__ nrm, const float* __restrict__ depth,
+                                   const int32_t* __restrict__ mat, int n_mat, const int32_t* __restrict__ mkind,
+                                   const float* __restrict__ malb, const float* __restrict__ mrough,
+                                   const float* __restrict__ view, const float* __restrict__ motion,
+                                   const uint8_t* __restrict__ hist, uint8_t* flags, float4* nd, float4* pr,
+                                   float4* va, float4* am) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  const int m = mat[i];
+  const bool has = m >= 0 && m < n_mat;
+  const int k = has ? mkind[m] : 0;
+  const float ar = has ? malb[3 * m] : 0.f, ag = has ? malb[3 * m + 1] : 0.f, ab = has ? malb[3 * m + 2] : 0.f;
+  const float ro = has ? mrough[m] : 0.f;
+  const uint8_t v = valid[i] ? 1 : 0;
+  const uint8_t h = (hist && hist[i]) ? 2 : 0;
+  const uint8_t g = (k == 1) ? 4 : 0;
+  flags[i] = v | h | g;
+  nd[i] = f4(nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2], depth[i]);
+  pr[i] = f4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], ro);
+  va[i] = f4(view[3 * i], view[3 * i + 1], view[3 * i + 2], ar);
+  am[i] = f4(ag, ab, motion ? motion[2 * i] : 0.f, motion ? motion[2 * i + 1] : 0.f);
+}
+
 __global__ void k_pack_vpl(int64_t p, const uint8_t* __restrict__ valid, const float* __restrict__ y,
                            const float* __restrict__ rad, const uint8_t* __restrict__ strat, float4* vy,
                            float4* vl) {
@@ -926,6 +954,23 @@ int pgg_pack_gbuffer(int64_t p, const uint8_t* valid, const float* pos, const fl
   if (const int rc = device_check()) return rc;
   k_pack_gbuffer<<<blocks(p, 256), 256, 0, S(stream)>>>(
       p, valid, pos, normal, depth, kind, albedo, rough, view, motion, has_history, flags,
+      reinterpret_cast<float4*>(nd), reinterpret_cast<float4*>(pr), reinterpret_cast<float4*>(va),
+      reinterpret_cast<float4*>(am));
+  return check_launch();
+}
+
+int pgg_pack_gbuffer_mat(int64_t p, const uint8_t* valid, const float* pos, const float* normal, const float* depth,
+                         const int32_t* mat, int32_t n_mat, const int32_t* mat_kind, const float* mat_albedo,
+                         const float* mat_rough, const float* view, const float* motion, const uint8_t* has_history,
+                         uint8_t* flags, float* nd, float* pr, float* va, float* am, void* stream) {
+  if (p < 0 || n_mat < 0 || !valid || !pos || !normal || !depth || !mat || !view || !flags || !nd || !pr || !va ||
+      !am)
+    return PGG_ERR_ARGUMENT;
+  if (n_mat > 0 && (!mat_kind || !mat_albedo || !mat_rough)) return PGG_ERR_ARGUMENT;
+  if (p == 0) return PGG_OK;
+  if (const int rc = device_check()) return rc;
+  k_pack_gbuffer_mat<<<blocks(p, 256), 256, 0, S(stream)>>>(
+      p, valid, pos, normal, depth, mat, n_mat, mat_kind, mat_albedo, mat_rough, view, motion, has_history, flags,
       reinterpret_cast<float4*>(nd), reinterpret_cast<float4*>(pr), reinterpret_cast<float4*>(va),
       reinterpret_cast<float4*>(am));
   return check_launch();

@@ -121,6 +121,31 @@ class GBufferPlanes:
         return g
 
     @classmethod
+    def pack_mat(cls, valid, pos, normal, depth, mat, mat_kind, mat_albedo, mat_rough, view, motion=None,
+                 has_history=None, cam_origin=(0.0, 0.0, 0.0), device="cuda", row0=0, stream=None):
+        """Like pack(), from the G-buffer's material ids (-1 = miss) and the
+        scene's material table (kind, albedo rgb, roughness per material):
+        the lookups of pg/ptrace.py:97-129 done on the device."""
+        def dev(a, dt):
+            if isinstance(a, np.ndarray):
+                a = torch.from_numpy(np.ascontiguousarray(a))
+            return a.to(device=device, dtype=dt).contiguous()
+
+        v = dev(valid, torch.uint8)
+        rows, w = v.shape
+        g = cls.empty(rows, w, device, row0)
+        g.cam_origin = tuple(float(c) for c in np.asarray(cam_origin, dtype=np.float64).reshape(3))
+        mk, ma, mr = dev(mat_kind, torch.int32), dev(mat_albedo, F32), dev(mat_rough, F32)
+        args = [dev(pos, F32), dev(normal, F32), dev(depth, F32), dev(mat, torch.int32)]
+        tail = [dev(view, F32), dev(motion, F32) if motion is not None else None,
+                dev(has_history, torch.uint8) if has_history is not None else None]
+        _lib.check(_lib.lib().pgg_pack_gbuffer_mat(
+            rows * w, _lib.ptr(v), *[_lib.ptr(a) for a in args], int(mk.numel()), _lib.ptr(mk), _lib.ptr(ma),
+            _lib.ptr(mr), *[_lib.ptr(a) for a in tail], _lib.ptr(g.flags), _lib.ptr(g.nd), _lib.ptr(g.pr),
+            _lib.ptr(g.va), _lib.ptr(g.am), _lib.stream_ptr(stream)))
+        return g
+
+    @classmethod
     def from_ref(cls, gb, device="cuda", row0=0, stream=None):
         """From a reference-style GBuffer object or dict."""
         get = (lambda k: gb[k]) if isinstance(gb, dict) else (lambda k: getattr(gb, k))

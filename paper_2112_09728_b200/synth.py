@@ -52,6 +52,12 @@ def _materials(seed, device):
     return kind.to(device), rough.to(device), albedo.to(device)
 
 
+def materials(seed=0, device="cpu"):
+    """The workload's material table: (kind int32, roughness, albedo rgb) per
+    material id -- what the G-buffer's kind / roughness / albedo look up."""
+    return _materials(seed, device)
+
+
 def _spheres(seed):
     g = torch.Generator(device="cpu").manual_seed(0x5F3E0000 + seed)
     cs, rs = [], []

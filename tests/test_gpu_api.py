@@ -240,3 +240,22 @@ def test_sgmap_lane_kernels(cuda_dev, kat):
         sgmap.hemisphere_to_square(np.array([[0.0, 0.0, -1.0]]))
     tp = torch.as_tensor(p[:10], device=cuda_dev)
     assert torch.is_tensor(sgmap.square_to_hemisphere(tp))
+
+
+def test_pack_gbuffer_mat_equals_pack(cuda_dev):
+    """pgg_pack_gbuffer_mat (material ids + the scene's material table, the
+    lookups of pg/ptrace.py:97-129) builds the same planes, bit for bit, as
+    pgg_pack_gbuffer from per-pixel kind / albedo / roughness -- misses
+    (mat -1) included; the e2e bench leg uploads this form."""
+    import torch
+
+    from paper_2112_09728_b200 import synth
+    from paper_2112_09728_b200.layout import GBufferPlanes
+    (_, _), (g, _) = list(synth.sequence(320, 180, 2, seed=3, device=cuda_dev))
+    assert (g["mat"] < 0).any() and (g["has_history"]).any()
+    a = GBufferPlanes.from_ref(g, device=cuda_dev)
+    kind, rough, alb = synth.materials(3, cuda_dev)
+    b = GBufferPlanes.pack_mat(g["valid"], g["pos"], g["normal"], g["depth"], g["mat"], kind, alb, rough, g["view"],
+                               g["motion"], g["has_history"], g["cam_origin"], device=cuda_dev)
+    for k in ("flags", "nd", "pr", "va", "am"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k
