@@ -61,6 +61,9 @@ constexpr int MAX_TILE_R = 12;  // EM halo staged in shared memory up to this ra
 #ifndef PGG_STASH
 #define PGG_STASH 1
 #endif
+#ifndef PGG_STAGE_KERNELS
+#define PGG_STAGE_KERNELS 1  // single-stage calls on stage-specialised instantiations
+#endif
 #ifndef PGG_MIN_BLOCKS
 #define PGG_MIN_BLOCKS 2  // 80 registers, 24 warps/SM with 32 x 12 tiles (round 1: 3 blocks of 32 x 8)
 #endif
@@ -118,7 +121,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // Measured alternatives (2/4/8 lanes per pixel with a butterfly reduction,
 // a split stage-1 / EM kernel pair) were slower; see DESIGN.md section 4.
 
-template <bool kTile, bool kFull>
+template <bool kTile, bool kFull, int kStage = 0>
 __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
     k_guiding_pass(const PassArgs A, const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmL,
                    int R) {
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SL.off_bar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int band_y0 = A.cfg.row0 + blockIdx.y * TILE_H;  // frame row of the tile's first row
-  if (kTile && A.has_vpl) {
+  if (kStage != 1 && kTile && A.has_vpl) {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -152,7 +155,10 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   S.flags = 0;
   S.nb = 0;
   bool train = false;
-  if (active) train = pixel_stage(A, x, yl, g0, g1, S);
+  if (active) train = pixel_stage<kStage>(A, x, yl, g0, g1, S);
+  if constexpr (kStage == 1) {
+    return;  // reprojection + sampling launch: no EM code at all
+  } else {
   if (!A.has_vpl) return;  // uniform across the grid
   if (!train) {
     S.flags = 0;
@@ -203,6 +209,7 @@ __global__ void __launch_bounds__(THREADS, PGG_MIN_BLOCKS)
   PGG_CHK(CHK_OUT, yl >= 0 && yl < A.cfg.rows && x < A.cfg.width, yl, x);
   st4(A.gout.g0, own, o0);
   st4(A.gout.g1, own, o1);
+  }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no
@@ -243,7 +250,7 @@ bool encode_vpl_map(CUtensorMap* m, const float* plane, int width, int rows, int
 // the (idempotent) attribute; the bit is published only after it succeeded.
 constexpr int MAX_DEVICES = 64;
 
-template <bool kTile, bool kFull>
+template <bool kTile, bool kFull, int kStage>
 int ensure_smem_opt_in(int dev) {
   static std::atomic<uint64_t> done{0};
   if (dev < 0 || dev >= MAX_DEVICES) return PGG_ERR_UNSUPPORTED;
@@ -251,7 +258,8 @@ int ensure_smem_opt_in(int dev) {
   if (done.load(std::memory_order_acquire) & bit) return PGG_OK;
   const SmemLayout big(kTile ? MAX_TILE_R : 0, kTile);  // the largest layout this instantiation can use
   const cudaError_t e =
-      cudaFuncSetAttribute(k_guiding_pass<kTile, kFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big.total);
+      cudaFuncSetAttribute(k_guiding_pass<kTile, kFull, kStage>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)big.total);
   if (e != cudaSuccess) {
     snprintf(g_cuda_err, sizeof(g_cuda_err), "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return PGG_ERR_CUDA;
@@ -260,28 +268,28 @@ int ensure_smem_opt_in(int dev) {
   return PGG_OK;
 }
 
-template <bool kTile, bool kFull>
+template <bool kTile, bool kFull, int kStage = 0>
 int launch_pass_t(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
   const SmemLayout SL(R, kTile);
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return check_launch();
-  const int rc = ensure_smem_opt_in<kTile, kFull>(dev);
+  const int rc = ensure_smem_opt_in<kTile, kFull, kStage>(dev);
   if (rc != PGG_OK) return rc;
   const dim3 grid((A.cfg.width + TILE_W - 1) / TILE_W, (A.cfg.rows + TILE_H - 1) / TILE_H);
-  k_guiding_pass<kTile, kFull><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
+  k_guiding_pass<kTile, kFull, kStage><<<grid, THREADS, SL.total, st>>>(A, my, ml, R);
   return check_launch();
 }
 
 // VPL planes that cover every candidate row of the launch (the whole frame,
 // or a row band with its full ceil(radius) halo) take the instantiation
 // without the per-candidate halo checks: no candidate can miss them
-template <bool kTile>
+template <bool kTile, int kStage = 0>
 int launch_pass(const PassArgs& A, const CUtensorMap& my, const CUtensorMap& ml, int R, cudaStream_t st) {
   const int halo = (int)ceil(A.cfg.radius > 0.0 ? A.cfg.radius : 0.0);
   const int lo = std::max(0, A.cfg.row0 - halo);
   const int hi = std::min(A.cfg.height, A.cfg.row0 + A.cfg.rows + halo);
-  if (A.vpl.row0 <= lo && A.vpl.row0 + A.vpl.rows >= hi) return launch_pass_t<kTile, true>(A, my, ml, R, st);
-  return launch_pass_t<kTile, false>(A, my, ml, R, st);
+  if (A.vpl.row0 <= lo && A.vpl.row0 + A.vpl.rows >= hi) return launch_pass_t<kTile, true, kStage>(A, my, ml, R, st);
+  return launch_pass_t<kTile, false, kStage>(A, my, ml, R, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -843,9 +851,22 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   CUtensorMap my, ml;
   memset(&my, 0, sizeof(my));
   memset(&ml, 0, sizeof(ml));
-  if (vpl && R <= MAX_TILE_R && encode_vpl_map(&my, vpl->y, cfg->width, vpl->rows, R) &&
-      encode_vpl_map(&ml, vpl->L, cfg->width, vpl->rows, R))
-    return launch_pass<true>(A, my, ml, R, S(stream));
+  const bool tile = vpl && R <= MAX_TILE_R && encode_vpl_map(&my, vpl->y, cfg->width, vpl->rows, R) &&
+                    encode_vpl_map(&ml, vpl->L, cfg->width, vpl->rows, R);
+#if PGG_STAGE_KERNELS
+  // single-stage calls take instantiations holding only their stages' code:
+  // training alone (training_pass, the frame loop's EM launch) without the
+  // sampler's state (no EM-loop spills), reprojection / sampling alone
+  // without the EM loop.  Calls with both halves stay fused: as two launches
+  // the latency-bound first half runs alone (0.514 vs 0.436 ms at 1080p,
+  // bitwise the same results).
+  if (A.has_vpl && !A.has_prev && !A.has_smp) {
+    if (tile) return launch_pass<true, 2>(A, my, ml, R, S(stream));
+    return launch_pass<false, 2>(A, my, ml, 0, S(stream));
+  }
+  if (!A.has_vpl) return launch_pass_t<false, false, 1>(A, my, ml, 0, S(stream));
+#endif
+  if (tile) return launch_pass<true>(A, my, ml, R, S(stream));
   return launch_pass<false>(A, my, ml, 0, S(stream));
 }
 

@@ -1146,6 +1146,10 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
 // Returns false when the pixel has nothing to train (invalid G-buffer:
 // Gamma passes through unchanged, guide_buffers.py:279-280).
 
+// kStage: 0 every stage the arguments select (the fused pass), 1 reprojection
+// + depth-0 sampling only (no EM code), 2 EM only (no reprojection or
+// sampling code; Gamma from gin).  The split launches 1 then 2.
+template <int kStage = 0>
 PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1, EmSetup& S) {
   const pgg_config& C = A.cfg;
   const int W = C.width;
@@ -1164,7 +1168,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
 #ifdef PGG_PROF_NO_REPROJ
   if (false) {  // measurement-only build
 #else
-  if (A.has_prev) {
+  if (kStage != 2 && A.has_prev) {
 #endif
     reproject_px(A, x, y, fl, nd, pr, am, g0, g1);
   } else {
@@ -1181,7 +1185,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
   S.nb = 0;
   if (!A.has_smp && !A.has_vpl) return false;
   if (!valid) {
-    if (A.has_smp) {
+    if (kStage != 2 && A.has_smp) {
       for (int s = 0; s < C.spp; ++s) {
         st4(A.smp.dir, own * C.spp + s, f4(0, 0, 0, 0));
         A.smp.tag[own * C.spp + s] = 0;
@@ -1202,7 +1206,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
 #ifdef PGG_PROF_NO_SMP
   if (false) {  // measurement-only build
 #else
-  if (A.has_smp) {
+  if (kStage != 2 && A.has_smp) {
 #endif
 #ifdef PGG_PROF_NO_GUIDE
     const bool guided = false;  // measurement-only build
@@ -1235,7 +1239,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
       A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
     }
   }
-  if (!A.has_vpl) return false;
+  if (kStage == 1 || !A.has_vpl) return false;
 #if PGG_SHARE_LANE_HASH
   em_setup(pr, va, am, glossy, pf, L, g1.w, C.k_max, splitmix64(C.key_train ^ hpix) * PCG_MUL + PCG_INC, S);
 #else
