@@ -1146,9 +1146,48 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
 // Returns false when the pixel has nothing to train (invalid G-buffer:
 // Gamma passes through unchanged, guide_buffers.py:279-280).
 
+// Depth-0 samples of one pixel's spp lanes (ptrace.py:161-220, 449-475).
+PGG_HD void sample_pixel(const PassArgs& A, int64_t own, uint64_t pix, const PixelFrame& pf, bool glossy,
+                         float rough, const LobeF& L, const float4& g0, const float4& g1) {
+  const pgg_config& C = A.cfg;
+#ifdef PGG_PROF_NO_GUIDE
+  const bool guided = false;  // measurement-only build
+#else
+  const bool guided = (!glossy || (double)rough >= C.rough_min_guide) && g1.w >= 1.0f;
+#endif
+  CholD cd;
+  cd.mx = g0.x;
+  cd.my = g0.y;
+  cd.m2xx = g0.z;
+  cd.m2yy = g0.w;
+  cd.m2xy = g1.x;
+  cd.from_floats = 0;
+#if PGG_SHARE_LANE_HASH
+  const uint64_t hpix = splitmix64(pix);
+#endif
+  for (int s = 0; s < C.spp; ++s) {
+#if PGG_SHARE_LANE_HASH
+    // spp == 1: the sampling lane key equals the pixel key of the EM stream
+    uint64_t st = (C.spp == 1 ? splitmix64(C.key_sample ^ hpix)
+                              : splitmix64(C.key_sample ^ splitmix64(pix * (uint64_t)C.spp + (uint64_t)s))) *
+                      PCG_MUL + PCG_INC;
+#else
+    uint64_t st = pcg_lane(C.key_sample, pix * (uint64_t)C.spp + (uint64_t)s);
+#endif
+    if (C.nee_draws == 3) {
+      st = st * J3_MUL + J3_ADD;  // the three NEE draws as one jump
+    } else {
+      for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
+    }
+    const LaneOut o = sample_lane(pf, glossy, rough, guided, L, cd, st);
+    st4(A.smp.dir, own * C.spp + s, f4(o.wi.x, o.wi.y, o.wi.z, o.pdf));
+    A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
+  }
+}
+
 // kStage: 0 every stage the arguments select (the fused pass), 1 reprojection
 // + depth-0 sampling only (no EM code), 2 EM only (no reprojection or
-// sampling code; Gamma from gin).  The split launches 1 then 2.
+// sampling code; Gamma from gin).
 template <int kStage = 0>
 PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1, EmSetup& S) {
   const pgg_config& C = A.cfg;
@@ -1208,36 +1247,7 @@ PGG_HD bool pixel_stage(const PassArgs& A, int x, int yl, float4& g0, float4& g1
 #else
   if (kStage != 2 && A.has_smp) {
 #endif
-#ifdef PGG_PROF_NO_GUIDE
-    const bool guided = false;  // measurement-only build
-#else
-    const bool guided = (!glossy || (double)rough >= C.rough_min_guide) && g1.w >= 1.0f;
-#endif
-    CholD cd;
-    cd.mx = g0.x;
-    cd.my = g0.y;
-    cd.m2xx = g0.z;
-    cd.m2yy = g0.w;
-    cd.m2xy = g1.x;
-    cd.from_floats = 0;
-    for (int s = 0; s < C.spp; ++s) {
-#if PGG_SHARE_LANE_HASH
-      // spp == 1: the sampling lane key equals the pixel key of the EM stream
-      uint64_t st = (C.spp == 1 ? splitmix64(C.key_sample ^ hpix)
-                                : splitmix64(C.key_sample ^ splitmix64(pix * (uint64_t)C.spp + (uint64_t)s))) *
-                        PCG_MUL + PCG_INC;
-#else
-      uint64_t st = pcg_lane(C.key_sample, pix * (uint64_t)C.spp + (uint64_t)s);
-#endif
-      if (C.nee_draws == 3) {
-        st = st * J3_MUL + J3_ADD;  // the three NEE draws as one jump
-      } else {
-        for (int k = 0; k < C.nee_draws; ++k) st = st * PCG_MUL + PCG_INC;
-      }
-      const LaneOut o = sample_lane(pf, glossy, rough, guided, L, cd, st);
-      st4(A.smp.dir, own * C.spp + s, f4(o.wi.x, o.wi.y, o.wi.z, o.pdf));
-      A.smp.tag[own * C.spp + s] = (uint8_t)(o.gauss | (o.valid << 1) | (o.draws << 2));
-    }
+    sample_pixel(A, own, pix, pf, glossy, rough, L, g0, g1);
   }
   if (kStage == 1 || !A.has_vpl) return false;
 #if PGG_SHARE_LANE_HASH
