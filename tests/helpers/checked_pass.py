@@ -83,6 +83,12 @@ for w, h in ((100, 70), (37, 29), (256, 64)):
             torch.cuda.synchronize()
             verify(full, rows)
             verify(full_r, rows, with_smp=False)
+            # training alone: the EM-only instantiations (kStage 2)
+            go2, _, full2 = guarded(rows, w, 2)
+            run_pass(cfg, 3, cur, gam, vpl=vp, row0=r0, rows=rows, height=h, want_samples=False, out_gamma=go2,
+                     halo_misses=miss)
+            torch.cuda.synchronize()
+            verify(full2, rows, with_smp=False)
         # stage-only calls
         gr, _, full_r = guarded(h, w, 2)
         run_pass(cfg, 3, cur, gam, prev=prev, want_reproj=True, want_samples=False, out_reproj=gr)
