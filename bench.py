@@ -1006,6 +1006,13 @@ def main():
                  "CUDA device(s) are visible")
     use_dist = world > 1 or args.bands or args.with_bands_leg
     if use_dist:
+        if "RANK" not in os.environ:  # one process without torchrun: a world of one
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
     __graft_entry__.build()
