@@ -138,7 +138,10 @@ typedef struct pgg_config {
  * gamma_prev / prev must hold every row a motion vector of the band reaches
  * (reprojection halo); vpl must hold the band +- rint(radius) rows clipped to
  * the frame (EM halo).  References outside the supplied rows are counted in
- * *halo_misses (device int32, may be NULL) and treated as out of frame. */
+ * *halo_misses (device int32, may be NULL) and treated as out of frame.
+ * With prev, gamma_out / gamma_reproj must not share planes with gamma_prev
+ * (reprojection reads other pixels' Gamma): PGG_ERR_ARGUMENT; without prev
+ * the update may be in place. */
 int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gbuffer* prev,
                      const pgg_gamma_in* gamma_prev, const pgg_vpl* vpl, const pgg_gamma_out* gamma_reproj,
                      const pgg_gamma_out* gamma_out, const pgg_samples* samples, int32_t* halo_misses,

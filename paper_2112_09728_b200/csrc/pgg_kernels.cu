@@ -829,6 +829,16 @@ int pgg_guiding_pass(const pgg_config* cfg, const pgg_gbuffer* cur, const pgg_gb
   if (!in_frame(cur->row0, cur->rows) || !in_frame(gamma_prev->row0, gamma_prev->rows)) return PGG_ERR_ARGUMENT;
   if (prev && !in_frame(prev->row0, prev->rows)) return PGG_ERR_ARGUMENT;
   if (vpl && !in_frame(vpl->row0, vpl->rows)) return PGG_ERR_ARGUMENT;
+  // reprojection reads Gamma at OTHER pixels (the motion source): an output
+  // plane that is also the input would race with it (without reprojection
+  // every pixel reads and writes only its own Gamma: in place is fine)
+  if (prev) {
+    const auto aliases = [&](const pgg_gamma_out* o) {
+      return o && (o->g0 == gamma_prev->g0 || o->g0 == gamma_prev->g1 || o->g1 == gamma_prev->g0 ||
+                   o->g1 == gamma_prev->g1);
+    };
+    if (aliases(gamma_out) || aliases(gamma_reproj)) return PGG_ERR_ARGUMENT;
+  }
   if (const int rc = device_check()) return rc;
   PassArgs A;
   memset(&A, 0, sizeof(A));

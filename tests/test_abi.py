@@ -53,6 +53,34 @@ def test_argument_errors_without_device(lib):
     assert lib.pgg_render_pass(None, None, None, None, None, None, None) == 1
 
 
+def test_reprojection_refuses_aliased_gamma(lib):
+    """With a previous G-buffer the pass reads Gamma at motion-source pixels:
+    an output plane shared with the input is refused before any launch (no
+    device needed); without reprojection in-place training is allowed past
+    this check (it then fails only for lack of a device)."""
+    import ctypes
+    from paper_2112_09728_b200 import _lib
+    cfg = _lib.Config()
+    cfg.width, cfg.height, cfg.row0, cfg.rows, cfg.spp, cfg.k_max = 64, 48, 0, 48, 1, 64
+    cfg.radius = 10.0
+    p = lambda a: ctypes.c_void_p(a)  # noqa: E731  (never dereferenced: refused before launch)
+    cur = _lib.GBuffer(p(0x1000), p(0x2000), p(0x3000), p(0x4000), p(0x5000), 0, 48)
+    prev = _lib.GBuffer(p(0x6000), p(0x7000), p(0x8000), p(0x9000), p(0xA000), 0, 48)
+    gin = _lib.GammaIn(p(0xB000), p(0xC000), 0, 48)
+    out_alias = _lib.GammaOut(p(0xC000), p(0xD000))
+    out_ok = _lib.GammaOut(p(0xE000), p(0xF000))
+    by = ctypes.byref
+    assert lib.pgg_guiding_pass(by(cfg), by(cur), by(prev), by(gin), None, None, by(out_alias), None, None,
+                                None) == 1
+    assert lib.pgg_guiding_pass(by(cfg), by(cur), by(prev), by(gin), None, by(out_alias), None, None, None,
+                                None) == 1
+    # not refused as an argument error (no CUDA device in this container)
+    assert lib.pgg_guiding_pass(by(cfg), by(cur), by(prev), by(gin), None, by(out_ok), None, None, None,
+                                None) != 1
+    assert lib.pgg_train(by(cfg), by(cur), by(gin), by(_lib.Vpl(p(0x11000), p(0x12000), 0, 48)),
+                         by(_lib.GammaOut(p(0xB000), p(0xC000))), None, None) != 1
+
+
 def test_struct_layout_matches_header():
     import ctypes
     from paper_2112_09728_b200 import _lib
