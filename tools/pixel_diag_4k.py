@@ -14,9 +14,11 @@ from paper_2112_09728_b200.session import GuidingSession, run_pass  # noqa: E402
 from test_gpu_pass import _ns, _samples  # noqa: E402
 
 Y, X = int(sys.argv[1]), int(sys.argv[2])
+SEED = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+FR = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 np.set_printoptions(precision=12, linewidth=160)
 dev = torch.device("cuda:0")
-w, h, seed, spp, F = 3840, 2160, 0, 4, 5
+w, h, seed, spp, F = 3840, 2160, SEED, 4, FR
 frames = list(synth.sequence(w, h, F, seed=seed, device=dev))
 cfg = PassConfig(seed=seed, spp=spp)
 sess = GuidingSession(w, h, cfg, device=dev)
