@@ -9,14 +9,19 @@ sys.path.insert(0, "tests")
 from helpers.full_frame import run  # noqa: E402
 
 recs = []
-cases = [(1920, 1080, 1, F, seed) for seed in (1, 2, 3) for F in (2, 6, 11, 16)]
-cases += [(3840, 2160, 4, 9, 1), (1280, 720, 2, 7, 5), (2560, 1440, 1, 5, 7)]
-for w, h, spp, F, seed in cases:
-    r = run(w, h, spp, F, seed=seed, verbose=False)
+if "--wide" in sys.argv:  # other pass parameters: spp, k_max, radius
+    cases = [(1920, 1080, spp, F, seed, kmax, rad) for seed in (11, 12) for F in (3, 9)
+             for spp, kmax, rad in ((2, 64, 10.0), (1, 32, 7.3), (4, 16, 12.0))]
+else:
+    cases = [(1920, 1080, 1, F, seed, 64, 10.0) for seed in (1, 2, 3) for F in (2, 6, 11, 16)]
+    cases += [(3840, 2160, 4, 9, 1, 64, 10.0), (1280, 720, 2, 7, 5, 64, 10.0), (2560, 1440, 1, 5, 7, 64, 10.0)]
+for w, h, spp, F, seed, kmax, rad in cases:
+    r = run(w, h, spp, F, seed=seed, verbose=False, k_max=kmax, radius=rad)
     r["seed"] = seed
     keys = ("gamma_rel_p9999", "gamma_rel_max", "k_mismatches", "strategy_mismatches", "valid_mismatches",
             "dir_abs_max", "pdf_rel_p9999", "pdf_rel_max")
-    print(json.dumps({"case": f"{w}x{h} spp{spp} F{F} seed{seed}", **{k: r[k] for k in keys}}), flush=True)
+    print(json.dumps({"case": f"{w}x{h} spp{spp} F{F} seed{seed} kmax{kmax} r{rad}", **{k: r[k] for k in keys}}),
+          flush=True)
     recs.append(r)
 summary = {
     "frames": len(recs),
