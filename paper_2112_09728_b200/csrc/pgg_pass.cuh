@@ -683,7 +683,7 @@ PGG_HD uint32_t pcg_out(uint64_t old) {
 // at cos = 1e-5, which moved one 4K pixel's Gamma by 8e-4 relative where that
 // record held the responsibility mass.
 #ifndef PGG_GRAZE
-#define PGG_GRAZE 1e-4f  // |cos| below which a record's cosine is re-evaluated in float64
+#define PGG_GRAZE 1e-3f  // |cos| below which a record's cosine is re-evaluated in float64
 #endif
 #ifndef PGG_GRAZE_FIX
 #define PGG_GRAZE_FIX 1

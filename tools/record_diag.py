@@ -17,7 +17,8 @@ from test_gpu_pass import _ns  # noqa: E402
 
 np.set_printoptions(precision=9, linewidth=180)
 dev = torch.device("cuda:0")
-w, h, seed, spp, F = 3840, 2160, 0, 4, 5
+import os
+w, h, seed, spp, F = (int(v) for v in os.environ.get("RD_CFG", "3840,2160,0,4,5").split(","))
 frames = list(synth.sequence(w, h, F, seed=seed, device=dev))
 sess = GuidingSession(w, h, PassConfig(seed=seed, spp=spp), device=dev)
 for f in range(F - 1):
