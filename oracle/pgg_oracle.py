@@ -685,7 +685,8 @@ def sample_frame(stats_f32, gbuf, seed, frame, spp=1, nee_draws=3, rough_min=ROU
 
 
 def guiding_frame(stats_prev_f32, gbuf_prev, gbuf, vpl, seed, frame, spp=1, nee_draws=3, kmax=KMAX,
-                  radius=RADIUS, depth_rel_tol=0.1, normal_dot_min=0.9, rough_min=ROUGH_MIN_GUIDE, rows=None):
+                  radius=RADIUS, depth_rel_tol=0.1, normal_dot_min=0.9, rough_min=ROUGH_MIN_GUIDE, rows=None,
+                  rotate_mean=True):
     """One full guiding pass in reference order: reproject (if history),
     depth-0 sampling on the reprojected Gamma, EM on the same Gamma with the
     frame's VPLs (pg/cli.py:114-142).  Returns (gamma_reproj, samples, gamma_trained).
@@ -695,7 +696,7 @@ def guiding_frame(stats_prev_f32, gbuf_prev, gbuf, vpl, seed, frame, spp=1, nee_
     if gbuf_prev is None:
         g = stats_prev_f32
     else:
-        g = reproject(stats_prev_f32, gbuf_prev, gbuf, depth_rel_tol, normal_dot_min)
+        g = reproject(stats_prev_f32, gbuf_prev, gbuf, depth_rel_tol, normal_dot_min, rotate_mean)
     smp = sample_frame(g, gbuf, seed, frame, spp, nee_draws, rough_min, rows=rows)
     g2 = train(g, vpl, gbuf, kmax, seed, frame, radius, rows=rows)
     if rows is not None:

@@ -115,3 +115,27 @@ def test_kmax_saturation(cuda_dev):
     got = _run(cuda_dev, gp, gc, vc, st, 5, 3, k_max=16)
     ref = _oracle(gp, gc, vc, st, 5, 3, kmax=16)
     check_gamma(got[2], ref[2])
+
+
+@pytest.mark.parametrize("gpu_kw,oracle_kw,spp", [
+    ({}, {}, 8),                                                            # many lanes per pixel
+    ({"nee_draws": 0}, {"nee_draws": 0}, 2),                                # scenes without emitters
+    ({"nee_draws": 5}, {"nee_draws": 5}, 1),                                # non-default NEE skip (no jump table)
+    ({"k_max": 1}, {"kmax": 1}, 1),                                         # eta = 1, budget 5 from k = 1 on
+    ({"depth_rel_tol": 0.01, "normal_dot_min": 0.99},
+     {"depth_rel_tol": 0.01, "normal_dot_min": 0.99}, 1),                   # strict reprojection gates
+    ({"roughness_min_guide": 0.0}, {"rough_min": 0.0}, 1),                  # every glossy lane guided
+    ({"roughness_min_guide": 0.9}, {"rough_min": 0.9}, 1),                  # almost none
+    ({"rotate_mean": False}, {"rotate_mean": False}, 1),                    # means carried unrotated
+])
+def test_pass_parameters_vs_oracle(cuda_dev, gpu_kw, oracle_kw, spp):
+    """Non-default pass parameters (pg/cli.py:34-77 RunConfig knobs) through
+    the fused pass against the oracle on a 48x40 frame with history: the
+    single-kernel policy on the reprojected and trained Gamma and the samples."""
+    gp, gc, vc, st = _inputs(48, 40, 7)
+    rep, smp, tr = _run(cuda_dev, gp, gc, vc, st, 4, 7, spp=spp, **gpu_kw)
+    orep, osmp, otr = _oracle(gp, gc, vc, st, 4, 7, spp=spp, **oracle_kw)
+    check_gamma(rep, orep)
+    check_gamma(tr, otr)
+    check_samples(smp, osmp["wi"].reshape(-1, spp, 3), osmp["pdf"].reshape(-1, spp), osmp["strategy"].reshape(-1, spp),
+                  osmp["valid"].reshape(-1, spp))
