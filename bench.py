@@ -1015,7 +1015,15 @@ def main():
                               MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import __graft_entry__
-    __graft_entry__.build()
+    if use_dist and world > 1:
+        # one compile per node: the other ranks wait, then find it up to date
+        if local_rank == 0:
+            __graft_entry__.build()
+        dist.barrier()
+        if local_rank != 0:
+            __graft_entry__.build()
+    else:
+        __graft_entry__.build()
     if args.seq:
         bench_sequence(args, rank, world, local_rank)
     elif args.bands or (world > 1 and args.workload != "1080p"):
