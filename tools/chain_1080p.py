@@ -22,6 +22,7 @@ from paper_2112_09728_b200.session import GuidingSession  # noqa: E402
 from helpers.full_frame import _ns  # noqa: E402
 
 G = {}
+EVERY = "--every" in sys.argv  # perturb by one ulp after EVERY frame (the kernel errs every step)
 
 
 def _train(rows):
@@ -67,7 +68,7 @@ def main(frames=16, ulp=False, out=None, w=1920, h=1080, seed=0):
             with mp.get_context("fork").Pool(os.cpu_count()) as pool:
                 parts = pool.map(_train, [(a, min(h, a + 24)) for a in range(0, h, 24)])
             gam = np.concatenate(parts, axis=0)
-            if rng is not None and f == 0:
+            if rng is not None and (f == 0 or EVERY):
                 sgn = rng.choice([-1.0, 1.0], size=gam[..., :6].shape).astype(np.float32)
                 gam[..., :6] = np.nextafter(gam[..., :6], gam[..., :6] + sgn)
             prev = gn
