@@ -344,6 +344,24 @@ PGG_HD uint64_t lcg_step(uint64_t s) {
 }
 static_assert((PCG_INC & 0xFFFFFFFFull) == 4150755663ull && (PCG_INC >> 32) == 335903614ull, "PCG increment halves");
 
+// s * M + C for compile-time (M, C) (a jump-ahead), carry-chained like lcg_step
+template <uint64_t M, uint64_t C> PGG_HD uint64_t lcg_jump(uint64_t s) {
+#if defined(__CUDA_ARCH__) && PGG_LCG_IMM
+  uint64_t r;
+  asm("{\n\t.reg .u64 m;\n\t.reg .u32 lo, hi;\n\t"
+      "mul.lo.u64 m, %1, %2;\n\t"
+      "mov.b64 {lo, hi}, m;\n\t"
+      "add.cc.u32 lo, lo, %3;\n\t"
+      "addc.u32 hi, hi, %4;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r)
+      : "l"(s), "n"(M), "n"((uint32_t)(C & 0xFFFFFFFFull)), "n"((uint32_t)(C >> 32)));
+  return r;
+#else
+  return s * M + C;
+#endif
+}
+
 PGG_HD uint32_t pcg_next(uint64_t& s) {
   const uint64_t old = s;
   s = lcg_step(old);
