@@ -555,6 +555,12 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
   return {(int)rint(rd * cos(ang)), (int)rint(rd * sin(ang))};
 }
 
+#ifndef PGG_GAUSS_FMA
+#define PGG_GAUSS_FMA 0  // 1: z by three FFMAs on pre-multiplied constants: -0.17 %, golden Gamma p99.99 2.7e-5 -> 3.6e-5 (not kept)
+#endif
+#ifndef PGG_W_UMASK
+#define PGG_W_UMASK 1  // record weight test 0 < w <= FLT_MAX as one unsigned compare of the bits
+#endif
 #ifndef PGG_GGX_LA
 #define PGG_GGX_LA 1  // GGX record weight as la + (luminance(L) - la) f5 (3 per-pixel invariants fewer): -0.45 %
 #endif
@@ -651,6 +657,19 @@ struct EmSetup {
   int nb;            // neighbour budget N (mixture.py:324-328)
   uint64_t s0;       // EM stream (seed, frame, pixel, stream_id=1)
 };
+
+// standardised square coordinates z = L^-1 (q - mu) (scaled by c) of a record
+PGG_HD void em_z(const EmSetup& S, float qx, float qy, float& z1, float& z2) {
+#if PGG_GAUSS_FMA
+  // z1 = qx il11 - mx il11, z2 = qy il22 - my il22 - (l21 il22) z1: three
+  // fused multiply-adds on pre-multiplied per-pixel constants
+  z1 = fmaf(qx, S.il11, -S.mx);
+  z2 = fmaf(qy, S.il22, fmaf(-S.l21, z1, -S.my));
+#else
+  z1 = (qx - S.mx) * S.il11;
+  z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+#endif
+}
 
 // jump table: state after n LCG steps is J_MUL[n] * s + J_ADD[n], n = 0..37
 // (every draw position of the 38-draw EM candidate block)
@@ -834,8 +853,8 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
     if (!kAll && !(isfinite(o.w) && o.w >= 0.0f)) return true;  // dropped by the M-step
   }
   dir_to_sq_f(dl, o.qx, o.qy);
-  const float z1 = (o.qx - S.mx) * S.il11;
-  const float z2 = ((o.qy - S.my) - S.l21 * z1) * S.il22;
+  float z1, z2;
+  em_z(S, o.qx, o.qy, z1, z2);
   const float num = S.pg * f_exp2(-(z1 * z1 + z2 * z2));
   const float den = num + S.qpi * bp;
   o.r = num * f_rcp(fmaxf(den, 1e-30f));  // den = 0 only with num = 0 -> r = 0
@@ -909,11 +928,17 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
 #endif
   }
   // non-finite or zero weights are dropped / add nothing (mixture.py:291)
+#if PGG_W_UMASK && defined(__CUDA_ARCH__)
+  // 0 < w <= FLT_MAX as one unsigned compare of the bits (negative, +-0,
+  // inf and NaN fall outside)
+  ok = ok && (__float_as_uint(w) - 1u) < 0x7F7FFFFFu;
+#else
   ok = ok && w > 0.0f && w <= 3.402823466e38f;
+#endif
   float qx, qy;
   dir_to_sq_f(dl, qx, qy);
-  const float z1 = (qx - S.mx) * S.il11;
-  const float z2 = ((qy - S.my) - S.l21 * z1) * S.il22;
+  float z1, z2;
+  em_z(S, qx, qy, z1, z2);
 #if PGG_LOOP_TRIM
   // -(z1^2 + z2^2) with the negation folded into the products (same value);
   // r is finite, so the masked w r is 0 * r = 0 as before
@@ -958,6 +983,9 @@ PGG_HD void em_record(const EmSetup& S, const float4& vy, const VS& V, int cx, i
 // 0.4967 vs 0.4725 ms -- slower, also at 2 blocks/SM without spills
 // (0.4966 ms); off.  DESIGN.md section 4.
 #define PGG_EM_PAIR 0
+#endif
+#if PGG_GAUSS_FMA && PGG_EM_PAIR == 2
+#error "PGG_GAUSS_FMA changes the EmSetup constants the pair path reads"
 #endif
 }  // namespace pgg
 #include "pgg_pair.cuh"
@@ -1149,12 +1177,21 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.a2 = alpha * alpha;
   S.kappa = kappa_world(pf.om_nn, S.a2);
   S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
+  // exponent -(z1^2 + z2^2)/2 evaluated as exp2(-(z1'^2 + z2'^2)) with z' = c z
+  const double il11c = (double)L.il11 * GAUSS_C, il22c = (double)L.il22 * GAUSS_C;
+  const double l21c = (double)L.l21 * (1.0 / GAUSS_C);  // constant reciprocal: no float64 division
+  S.il11 = (float)il11c;
+  S.il22 = (float)il22c;
+#if PGG_GAUSS_FMA
+  // em_z's fused form: mu and the cross term pre-multiplied
+  S.mx = (float)((double)L.mx * il11c);
+  S.my = (float)((double)L.my * il22c);
+  S.l21 = (float)(l21c * il22c);
+#else
   S.mx = L.mx;
   S.my = L.my;
-  // exponent -(z1^2 + z2^2)/2 evaluated as exp2(-(z1'^2 + z2'^2)) with z' = c z
-  S.il11 = (float)((double)L.il11 * GAUSS_C);
-  S.l21 = (float)((double)L.l21 * (1.0 / GAUSS_C));  // constant reciprocal: no float64 division
-  S.il22 = (float)((double)L.il22 * GAUSS_C);
+  S.l21 = (float)l21c;
+#endif
   S.pg = L.pi * L.gnorm;
   S.qpi = 1.0f - L.pi;
   S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
