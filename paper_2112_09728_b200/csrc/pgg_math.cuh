@@ -542,6 +542,12 @@ PGG_HD float atan4pi_unit(float t) {
   p = fmaf(p, u, 1.2732386589050293f);
   return t * p;
 }
+#ifndef PGG_SQ_NOFLOOR
+#define PGG_SQ_NOFLOOR 1  // no 1e-30 floor under the lift rsqrt (the saturating clip maps the z = -1 inf / NaN to 0): -0.2 %, same Gamma
+#endif
+#ifndef PGG_SQ_MUFU_SQRT
+#define PGG_SQ_MUFU_SQRT 0  // 1: rho on MUFU.SQRT: a further -0.6 % but golden Gamma p99.99 2.7e-5 -> 4.0e-5 (not kept)
+#endif
 #ifndef PGG_SQ_FMA_SAT
 #define PGG_SQ_FMA_SAT 1  // record square map clip as fma.sat (one FFMA.SAT instead of FFMA + FADD.SAT): with PGG_W_UMASK -0.7 %, same Gamma
 #endif
@@ -549,7 +555,11 @@ PGG_HD float atan4pi_unit(float t) {
 #define PGG_SQ_RAW 1  // record square mapping on raw MUFU rsqrt / rcp: 0.528 -> 0.519 ms; golden Gamma p99.99 stays <= 3.1e-5 (limit 1e-4)
 #endif
 PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
-#if defined(__CUDA_ARCH__) && PGG_SQ_RAW
+#if defined(__CUDA_ARCH__) && PGG_SQ_RAW && PGG_SQ_NOFLOOR
+  // no floor: 1 + z <= 0 (z = -1, masked records only) gives inf / NaN,
+  // which the saturating clip below maps to finite 0
+  const float rs = rsqrtf(1.0f + v.z);
+#elif defined(__CUDA_ARCH__) && PGG_SQ_RAW
   const float rs = rsqrtf(fmaxf(1.0f + v.z, 1e-30f));
 #else
   const float rs = r_rsqrt(fmaxf(1.0f + v.z, 1e-30f));
@@ -559,7 +569,11 @@ PGG_HD void dir_to_sq_f(const V3<float>& v, float& sx, float& sy) {
   const float rho2 = x * x + y * y;
 #if defined(__CUDA_ARCH__) && PGG_SQ_RAW
   // floors instead of guards: a zero rho2 / max gives 0 * finite = 0
+#if PGG_SQ_MUFU_SQRT
+  const float rho = f_sqrt_mufu(rho2);  // MUFU.SQRT (sqrt.approx; 0 -> 0)
+#else
   const float rho = rho2 * rsqrtf(fmaxf(rho2, 1e-36f));
+#endif
   const float mx = fmaxf(ax, ay);
   const float t = fminf(ax, ay) * f_rcp(fmaxf(mx, 1e-36f));
 #else
