@@ -13,7 +13,7 @@ SRC = {"pgg_math.cuh": "paper_2112_09728_b200/csrc/pgg_math.cuh",
 def starts(path):
     out = []
     for i, l in enumerate(open(path).read().splitlines(), 1):
-        m = re.match(r"^(?:template <[^>]*>\s*)?(?:PGG_HD|PGG_COLD|PGG_MHD|PGG_PI|__global__|__device__|int |static )"
+        m = re.match(r"^\s*(?:template <[^>]*>\s*)?(?:PGG_HD|PGG_COLD|PGG_MHD|PGG_PI|__global__|__device__|int |static )"
                      r"[\w:<>,\s&*]*?\b(\w+)\(", l)
         if m:
             out.append((i, m.group(1)))
