@@ -650,8 +650,12 @@ def bench_ours(args, rank, world, local_rank):
         frames.clear()
         torch.cuda.empty_cache()
         w4, h4, spp4, _ = WORKLOADS["4k4spp"]
-        bands = bench_bands(args, rank, world, local_rank, w4, h4, spp4, max(8, min(args.steps, 32)),
-                            max(3, args.warmup), "4k4spp")
+        try:
+            bands = bench_bands(args, rank, world, local_rank, w4, h4, spp4, max(8, min(args.steps, 32)),
+                                max(3, args.warmup), "4k4spp")
+        except Exception as e:  # the headline line must not be lost to the extra leg
+            bands = {"error": f"{type(e).__name__}: {e}"[:300]}
+            print(f"bench.py: rank {rank}: bands_4k4spp leg failed: {bands['error']}", file=sys.stderr, flush=True)
     cpu = None
     c0 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "1080p":
