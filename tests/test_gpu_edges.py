@@ -1,7 +1,8 @@
 """Edge cases of the fused pass against the oracle: partial
 tiles and tiny frames, a neighbour radius beyond the shared-memory tile
 (global VPL path), radius 0 (every candidate is the pixel itself), 4 spp,
-all-invalid G-buffers, no history, and sequences trained past k_max."""
+all-invalid G-buffers, no history, sequences trained past k_max, and VPLs
+behind the receiver, in its tangent plane or on it."""
 
 from types import SimpleNamespace
 
@@ -105,6 +106,33 @@ def test_no_history_resets(cuda_dev):
     v = gc["valid"].cpu().numpy().astype(bool)
     fresh = O.fresh_stats(1).astype(np.float32)[0]
     assert (got[0][v] == fresh).all()  # every valid pixel starts from init_stats
+    check_gamma(got[2], ref[2])
+
+
+def test_vpls_behind_and_in_the_tangent_plane(cuda_dev):
+    """Records the reference masks or re-decides: VPLs straight behind the
+    receiver (own record along -n: the square map's 1 + z reaches 0, masked)
+    and VPLs in the receiver's tangent plane (cosine ~0: the float64 cosine
+    path), mixed with ordinary ones."""
+    gp, gc, vc, st = _inputs(48, 32, seed=21)
+    vc = dict(vc)
+    pos, n = gc["pos"], gc["normal"]
+    y = vc["y"].clone()
+    h, w = pos.shape[:2]
+    sel = torch.zeros(h, w, dtype=torch.long)
+    sel[::2, ::2] = 1  # behind
+    sel[1::2, 1::2] = 2  # tangent plane: pos + (n x helper) * 1.5
+    behind = pos - 2.0 * n
+    helper = torch.tensor([0.0, 0.0, 1.0]).expand_as(n)
+    t = torch.cross(n, helper, dim=-1)
+    t = t / torch.clamp(torch.sqrt((t * t).sum(-1, keepdim=True)), min=1e-12)
+    tangent = pos + 1.5 * t
+    y = torch.where((sel == 1)[..., None], behind, y)
+    y = torch.where((sel == 2)[..., None], tangent, y)
+    vc["y"] = y
+    got = _run(cuda_dev, gp, gc, vc, st, 4, 9)
+    assert np.isfinite(got[2]).all()
+    ref = _oracle(gp, gc, vc, st, 4, 9)
     check_gamma(got[2], ref[2])
 
 
