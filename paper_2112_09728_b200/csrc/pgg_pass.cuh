@@ -555,6 +555,19 @@ PGG_COLD Off2 disk_offset_d(uint32_t ua, uint32_t ub, double radius) {
   return {(int)rint(rd * cos(ang)), (int)rint(rd * sin(ang))};
 }
 
+#ifndef PGG_PI_FOLD
+#define PGG_PI_FOLD 0  // 1: one multiply fewer per Lambert record; measured neutral (0.4276 vs 0.4276 ms), not kept
+#endif
+#if PGG_PI_FOLD
+// 1/pi folded into the per-pixel constants (albedo, 1 - pi) and pi into G1(wo):
+// the records' bp carries pi x the BRDF pdf and the Lambert bp is cos itself
+constexpr float kLumR = (float)(0.2126 / 3.14159265358979323846), kLumG = (float)(0.7152 / 3.14159265358979323846),
+                kLumB = (float)(0.0722 / 3.14159265358979323846);
+#define PGG_LAMBERT_BP(cr) (cr)
+#else
+constexpr float kLumR = 0.2126f, kLumG = 0.7152f, kLumB = 0.0722f;
+#define PGG_LAMBERT_BP(cr) ((cr) * K<float>::inv_pi)
+#endif
 #ifndef PGG_GAUSS_FMA
 #define PGG_GAUSS_FMA 0  // 1: z by three FFMAs on pre-multiplied constants: -0.17 %, golden Gamma p99.99 2.7e-5 -> 3.6e-5 (not kept)
 #endif
@@ -831,7 +844,7 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
     const float4 lv = V.get_L(cx, cy);
     if (!(S.flags & 2)) {
       // Lambert: luminance(L albedo / pi) cos, pdf cos / pi (scene.py:269, 296)
-      bp = cr * K<float>::inv_pi;
+      bp = PGG_LAMBERT_BP(cr);
       o.w = (lv.x * S.alb_r + lv.y * S.alb_g + lv.z * S.alb_b) * bp;
     } else {
       // GGX (scene.py:271-283, 298-307); G1(wo)/(4 cos_o) is a pixel constant
@@ -844,9 +857,9 @@ PGG_HD bool em_eval(const EmSetup& S, const float4& vy, const VS& V, int cx, int
       const float t2 = t * t;
       const float f5 = t2 * t2 * t;
       // luma_c F_c = la_c + (luma_c - la_c) f5 (Schlick, F0 = albedo)
-      const float kr = fmaf(0.2126f - S.alb_r, f5, S.alb_r);
-      const float kg = fmaf(0.7152f - S.alb_g, f5, S.alb_g);
-      const float kb = fmaf(0.0722f - S.alb_b, f5, S.alb_b);
+      const float kr = fmaf(kLumR - S.alb_r, f5, S.alb_r);
+      const float kg = fmaf(kLumG - S.alb_g, f5, S.alb_g);
+      const float kb = fmaf(kLumB - S.alb_b, f5, S.alb_b);
       // f cos = F D G1(wi) G1(wo) / (4 cos_i cos_o) * cos_i
       o.w = (lv.x * kr + lv.y * kg + lv.z * kb) * spec;
     }
@@ -901,7 +914,7 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
 #endif
   const float4 lv = V.L_at(idx);
   // Lambert (scene.py:269, 296)
-  float bp = cr * K<float>::inv_pi;
+  float bp = PGG_LAMBERT_BP(cr);
   // S.alb_c = luminance weight x albedo: la = luminance(L albedo)
   const float la = lv.x * S.alb_r + lv.y * S.alb_g + lv.z * S.alb_b;
   float w = la * bp;
@@ -918,12 +931,12 @@ PGG_HD void em_accumulate(const EmSetup& S, const float4& vy, const VS& V, IDX i
 #if PGG_GGX_LA
     // luminance(L F), Schlick F_c = albedo_c + (1 - albedo_c) f5, as
     // la + (luminance(L) - la) f5: no per-pixel (lum_c - albedo_c) invariants
-    const float ll = fmaf(0.0722f, lv.z, fmaf(0.7152f, lv.y, 0.2126f * lv.x));
+    const float ll = fmaf(kLumB, lv.z, fmaf(kLumG, lv.y, kLumR * lv.x));
     w = fmaf(ll - la, f5, la) * spec;
 #else
-    const float kr = fmaf(0.2126f - S.alb_r, f5, S.alb_r);
-    const float kg = fmaf(0.7152f - S.alb_g, f5, S.alb_g);
-    const float kb = fmaf(0.0722f - S.alb_b, f5, S.alb_b);
+    const float kr = fmaf(kLumR - S.alb_r, f5, S.alb_r);
+    const float kg = fmaf(kLumG - S.alb_g, f5, S.alb_g);
+    const float kb = fmaf(kLumB - S.alb_b, f5, S.alb_b);
     w = (lv.x * kr + lv.y * kg + lv.z * kb) * spec;
 #endif
   }
@@ -1171,12 +1184,15 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.x = v3(pr.x, pr.y, pr.z);
   S.fr = pf.fr;
   S.wol = pf.wol;
-  S.alb_r = 0.2126f * va.w;
-  S.alb_g = 0.7152f * am.x;
-  S.alb_b = 0.0722f * am.y;
+  S.alb_r = kLumR * va.w;
+  S.alb_g = kLumG * am.x;
+  S.alb_b = kLumB * am.y;
   S.a2 = alpha * alpha;
   S.kappa = kappa_world(pf.om_nn, S.a2);
   S.g1o = glossy ? ggx_g1(S.a2, fabsf(pf.wol.z)) / fmaxf(4.0f * pf.wol.z, 1e-30f) : 0.0f;
+#if PGG_PI_FOLD
+  S.g1o *= 3.14159265358979323846f;
+#endif
   // exponent -(z1^2 + z2^2)/2 evaluated as exp2(-(z1'^2 + z2'^2)) with z' = c z
   const double il11c = (double)L.il11 * GAUSS_C, il22c = (double)L.il22 * GAUSS_C;
   const double l21c = (double)L.l21 * (1.0 / GAUSS_C);  // constant reciprocal: no float64 division
@@ -1193,7 +1209,11 @@ PGG_HD void em_setup(const float4& pr, const float4& va, const float4& am, bool 
   S.l21 = (float)l21c;
 #endif
   S.pg = L.pi * L.gnorm;
+#if PGG_PI_FOLD
+  S.qpi = (1.0f - L.pi) * K<float>::inv_pi;
+#else
   S.qpi = 1.0f - L.pi;
+#endif
   S.flags = 1 | (glossy ? 2 : 0) | (pf.co_pos ? 4 : 0);
   S.nb = neighbor_budget(k, kmax);
 #ifdef PGG_PROF_NO_EM
